@@ -1,0 +1,178 @@
+/*
+ * fusedmm_cuda.h — C ABI of libfusedmm_cuda, the sm_100a (B200) FusedMM path.
+ *
+ * Drop-in boundary for the reference's header-only kernel
+ *   template<class T> DenseMatrix<T> fusedmm::fused_mm(A, X, Y, spec, t, stats, opts)
+ *   (/root/reference/proj/include/fusedmm/kernel.hpp:297-353)
+ * and its five-slot operator interface OpSpec<T>{vop,rop,sop,mop,aop,alpha,...}
+ *   (/root/reference/proj/include/fusedmm/ops.hpp:12-51).
+ *
+ * Everything here is plain C: pointers, sizes, status codes. No torch / C++
+ * types cross this boundary. The C++ wrapper with the reference's exact
+ * signature and exception types is include/fusedmm_cuda.hpp; the Python mirror
+ * is paper_2011_06391_b200/fusedmm.py. Bindings a maintainer would add are in
+ * INTEGRATION.md.
+ *
+ * Semantics: Z[u,:] = AOP-fold over v in N(u), in CSR storage order, of
+ *   VOP(x_u, y_v) -> [ROP -> SOP(s, a_uv) -> MOP(h, y_v)]   (scalar message)
+ *                 -> [SOP elementwise -> MOP(t, y_v, a_uv)]  (vector message)
+ * exactly as fusedmm::update_u (kernel.hpp:81-107). There is no CPU fallback:
+ * a slot this library cannot run on the device returns FMM_E_UNSUPPORTED.
+ */
+#ifndef FUSEDMM_CUDA_H
+#define FUSEDMM_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMM_ABI_VERSION 1
+
+/* Status codes. FMM_E_INVAL maps to std::invalid_argument and FMM_E_LOGIC to
+ * std::logic_error in the C++ wrapper (kernel.hpp:272-281,303; ops.hpp:102-103). */
+typedef enum fmm_status {
+    FMM_OK = 0,
+    FMM_E_INVAL = 1,       /* bad argument / dimension mismatch / bad CSR   */
+    FMM_E_UNSUPPORTED = 2, /* USER slot or shape with no device kernel      */
+    FMM_E_CUDA = 3,        /* CUDA runtime error (message in last_error)    */
+    FMM_E_NCCL = 4,        /* reserved for the collective layer             */
+    FMM_E_OOM = 5,         /* device or pinned-host allocation failed       */
+    FMM_E_LOGIC = 6        /* contract violation inside the call            */
+} fmm_status;
+
+/* Slot codes keep the reference enum order (ops.hpp:14-18). Device-only
+ * extensions sit above the USER values; they express the "scale the VOP
+ * output" step (the paper's VSC) that the reference can only reach through a
+ * USER VOP lambda (SURVEY.md §8(a) "Oracle op definitions"). */
+enum {
+    FMM_VOP_ADD = 0, FMM_VOP_MUL = 1, FMM_VOP_SEL2ND = 2, FMM_VOP_SUB = 3,
+    FMM_VOP_USER = 4
+};
+enum {
+    FMM_ROP_NOOP = 0, FMM_ROP_RSUM = 1, FMM_ROP_RMUL = 2, FMM_ROP_NORM = 3,
+    FMM_ROP_USER = 4,
+    FMM_ROP_SQNORM = 16 /* s = sum_j t_j*t_j (no sqrt)                     */
+};
+enum {
+    FMM_SOP_NOOP = 0, FMM_SOP_SIGMOID = 1, FMM_SOP_SCAL = 2, FMM_SOP_USER = 3,
+    FMM_SOP_TDIST = 16, /* h = 1/(1+s)         (t-distribution kernel)      */
+    FMM_SOP_SQK = 17    /* h = s/k             (FR attractive, k = spec.k)  */
+};
+enum {
+    FMM_MOP_MUL = 0, FMM_MOP_SEL2ND = 1, FMM_MOP_USER = 2,
+    FMM_MOP_MUL_VOP = 16 /* w_j = a_uv*(h*t_j): scale the VOP output t     */
+};
+enum { FMM_AOP_ASUM = 0, FMM_AOP_AMAX = 1, FMM_AOP_USER = 2 };
+
+/* KnownPattern (ops.hpp:20) plus the two device-only patterns. */
+enum {
+    FMM_PATTERN_SIGMOID_EMBED = 0,
+    FMM_PATTERN_SPMM_GCN = 1,
+    FMM_PATTERN_FR_LAYOUT = 2,
+    FMM_PATTERN_GENERIC = 3,
+    FMM_PATTERN_TDIST = 16,      /* SUB,SQNORM,TDIST,MUL_VOP,ASUM (config 3) */
+    FMM_PATTERN_FR_ATTRACT = 17  /* SUB,SQNORM,SQK,MUL_VOP,ASUM   (config 4) */
+};
+
+/* POD mirror of OpSpec<float> without the std::function hooks. */
+typedef struct fmm_opspec {
+    int32_t vop, rop, sop, mop, aop;
+    float alpha; /* SCAL factor (ops.hpp:49)                  */
+    float k;     /* SQK divisor; ignored by the other ops      */
+} fmm_opspec;
+
+/* fmm_run / fmm_iterate flags. */
+enum {
+    FMM_HOST_PTRS = 0,         /* X, Y, Z are host pointers (default)       */
+    FMM_DEVICE_PTRS = 1u << 0, /* X, Y, Z are device pointers on shard 0's
+                                  device; single-shard contexts only        */
+    FMM_ASYNC = 1u << 1,       /* with FMM_DEVICE_PTRS: do not synchronize  */
+    FMM_EXACT = 1u << 2,       /* force bit-exact scheme    */
+    FMM_FAST = 1u << 3         /* force reassociating scheme (FMA, splits)  */
+};
+
+/* Mirrors KernelStats (kernel.hpp:51-55) plus device-side evidence. */
+typedef struct fmm_stats {
+    uint64_t aux_bytes;   /* device scratch held for the call (partials)    */
+    int32_t threads;      /* number of shards (GPUs) that ran                */
+    int32_t pattern;      /* FMM_PATTERN_*                                   */
+    int32_t exact;        /* 1 if the bit-exact scheme ran                   */
+    int32_t launches;     /* kernels launched by this call                   */
+    float kernel_ms;      /* device time of the fused kernels (shard max),
+                             measured with events on the launch stream; 0
+                             under FMM_ASYNC                                 */
+    float total_ms;       /* device time including host<->device copies     */
+} fmm_stats;
+
+/* Graph summary after upload (for tests and the bench's byte model). */
+typedef struct fmm_graph_info {
+    int64_t m, n, nnz;
+    int64_t row_begin, row_end; /* rows this graph object covers          */
+    int64_t nonempty_rows;
+    int64_t max_degree;
+    int64_t split_rows;         /* rows cut into chunks on the fast path  */
+    int64_t split_chunks;
+    int32_t shards;
+    int32_t has_values;
+} fmm_graph_info;
+
+typedef struct fmm_ctx fmm_ctx;
+typedef struct fmm_graph fmm_graph;
+
+const char* fmm_version(void);
+const char* fmm_status_string(fmm_status s);
+
+/* Context: one shard per entry of devs (duplicates allowed; they become
+ * independent shards on the same GPU, which is how the multi-shard exchange
+ * is exercised on one device). ngpu >= 1 mirrors `t >= 1` (kernel.hpp:303). */
+fmm_status fmm_create(int ngpu, const int* devs, fmm_ctx** out);
+fmm_status fmm_destroy(fmm_ctx* ctx);
+const char* fmm_last_error(const fmm_ctx* ctx);
+int fmm_device_count(void);
+
+/* Run shard i's kernels on an external stream (e.g. torch's current stream)
+ * instead of the context's own. stream is a cudaStream_t; NULL means the
+ * legacy default stream. fmm_reset_stream restores the context's own. */
+fmm_status fmm_set_stream(fmm_ctx* ctx, int shard, void* stream);
+fmm_status fmm_reset_stream(fmm_ctx* ctx, int shard);
+
+/* Host-side helpers, no device work. */
+fmm_status fmm_pattern_of(const fmm_opspec* spec, int32_t* pattern);
+/* part1d (kernel.hpp:24-49): boundaries[0..t], same greedy rule. */
+fmm_status fmm_part1d(int64_t m, const int64_t* row_ptr, int t,
+                      int64_t* boundaries);
+
+/* Upload A (CSR, host arrays, int64 indices as in matrix.hpp:48-68).
+ * Only rows [row_begin, row_end) are uploaded (pass 0, m for all rows); a
+ * multi-shard context further splits that range with part1d. values may be
+ * NULL (all a_uv = 1). Validates row_ptr monotone / col in [0, n). */
+fmm_status fmm_graph_upload(fmm_ctx* ctx, int64_t m, int64_t n,
+                            const int64_t* row_ptr, const int64_t* col_idx,
+                            const float* values, int64_t row_begin,
+                            int64_t row_end, fmm_graph** out);
+fmm_status fmm_graph_free(fmm_graph* g);
+fmm_status fmm_graph_get_info(const fmm_graph* g, fmm_graph_info* out);
+/* Boundaries of the shards (length shards+1, absolute row ids). */
+fmm_status fmm_graph_shard_bounds(const fmm_graph* g, int64_t* bounds);
+
+/* One fused call. X: m x d (rows indexed by absolute row id), Y: ny x d,
+ * Z: (row_end-row_begin) x d output for this graph's rows. Host pointers
+ * unless FMM_DEVICE_PTRS. stats may be NULL. */
+fmm_status fmm_run(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec,
+                   int64_t d, const float* X, int64_t ny, const float* Y,
+                   float* Z, uint32_t flags, fmm_stats* stats);
+
+/* iters fused calls with X <- Z between them (square A, Y = X), the Z slices
+ * exchanged between shards on the device. X is the host m x d input and
+ * receives the final iterate. */
+fmm_status fmm_iterate(fmm_ctx* ctx, const fmm_graph* g,
+                       const fmm_opspec* spec, int64_t d, float* X, int iters,
+                       uint32_t flags, fmm_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FUSEDMM_CUDA_H */

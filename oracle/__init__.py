@@ -1,0 +1,226 @@
+"""CPU oracle for the FusedMM hot path — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+legs may import this package, and only as the checker or the CPU baseline;
+the product (paper_2011_06391_b200, libfusedmm_cuda.so) never links or calls
+it and has no CPU fallback.
+
+Two checkers:
+  * libfmm_oracle.so — the C restatement (fmm_oracle.c), bit-for-bit the
+    reference's fused_mm<float>/<double> (kernel.hpp:297-353);
+  * libfusedmm_ref.so — the unmodified reference headers compiled in place
+    (oracle/_ref, built by oracle/Makefile when /root/reference exists),
+    used to pin the restatement and as the reference CPU baseline.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ORACLE_SO = HERE / "_build" / "libfmm_oracle.so"
+REF_SO = HERE / "_ref" / "libfusedmm_ref.so"
+
+P64 = C.POINTER(C.c_int64)
+PF = C.POINTER(C.c_float)
+PD = C.POINTER(C.c_double)
+
+
+class or_spec(C.Structure):
+    _fields_ = [("vop", C.c_int32), ("rop", C.c_int32), ("sop", C.c_int32), ("mop", C.c_int32),
+                ("aop", C.c_int32), ("alpha", C.c_double), ("k", C.c_double)]
+
+
+def _spec(spec) -> or_spec:
+    return or_spec(int(spec.vop), int(spec.rop), int(spec.sop), int(spec.mop), int(spec.aop),
+                   float(np.float32(spec.alpha)), float(np.float32(spec.k)))
+
+
+_or = None
+_ref = None
+
+
+def oracle_lib() -> C.CDLL:
+    global _or
+    if _or is None:
+        if not ORACLE_SO.exists():
+            raise ImportError(f"{ORACLE_SO} missing: run `make -C oracle`")
+        L = C.CDLL(str(ORACLE_SO))
+        args = [C.c_int64, C.c_int64, P64, P64, None, C.c_int64, None, C.c_int64, None,
+                C.POINTER(or_spec), C.c_int, C.c_int, P64, C.c_int64, None]
+        L.fmm_oracle_fused_mm_f32.argtypes = [PF if a is None else a for a in args]
+        L.fmm_oracle_fused_mm_f64.argtypes = [PD if a is None else a for a in args]
+        L.fmm_oracle_part1d.argtypes = [C.c_int64, P64, C.c_int, P64]
+        L.fmm_oracle_pattern_of.argtypes = [C.POINTER(or_spec)]
+        _or = L
+    return _or
+
+
+def ref_available() -> bool:
+    return REF_SO.exists()
+
+
+def ref_lib() -> C.CDLL:
+    global _ref
+    if _ref is None:
+        if not REF_SO.exists():
+            raise ImportError(f"{REF_SO} missing: build with `make -C oracle` where /root/reference exists")
+        L = C.CDLL(str(REF_SO))
+        L.fmm_ref_prepare_f32.restype = C.c_void_p
+        L.fmm_ref_prepare_f32.argtypes = [C.c_int64, C.c_int64, P64, P64, PF, C.c_int64, PF, C.c_int64,
+                                          PF, C.POINTER(or_spec), C.c_int]
+        L.fmm_ref_run_f32.argtypes = [C.c_void_p, C.c_int, PF, PD]
+        L.fmm_ref_release_f32.argtypes = [C.c_void_p]
+        L.fmm_ref_prepare_f64.restype = C.c_void_p
+        L.fmm_ref_prepare_f64.argtypes = [C.c_int64, C.c_int64, P64, P64, PD, C.c_int64, PD, C.c_int64,
+                                          PD, C.POINTER(or_spec), C.c_int]
+        L.fmm_ref_run_f64.argtypes = [C.c_void_p, C.c_int, PD, PD]
+        L.fmm_ref_release_f64.argtypes = [C.c_void_p]
+        L.fmm_ref_unfused_f32.argtypes = [C.c_void_p, PF]
+        L.fmm_ref_part1d.argtypes = [C.c_int64, P64, C.c_int, P64]
+        L.fmm_ref_rmat.restype = C.c_int64
+        L.fmm_ref_rmat.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_uint64,
+                                   P64, P64, PF]
+        L.fmm_ref_pattern_of.argtypes = [C.POINTER(or_spec)]
+        _ref = L
+    return _ref
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def _arrs(A, X, Y, f64: bool):
+    dt = np.float64 if f64 else np.float32
+    Xa = np.ascontiguousarray(X.data if hasattr(X, "data") else X, dtype=dt).reshape(-1)
+    Ya = Xa if (Y is X) else np.ascontiguousarray(Y.data if hasattr(Y, "data") else Y, dtype=dt).reshape(-1)
+    V = None if getattr(A, "unit_values", False) else np.ascontiguousarray(A.values, dtype=dt)
+    return Xa, Ya, V
+
+
+def oracle_fused_mm(A, X, Y, spec, threads: int | None = None, lane_width: int = 8, rows=None,
+                    f64: bool = False) -> np.ndarray:
+    """fused_mm<float> (or <double> with f64=True) over all rows, or only the
+    selected `rows` (output row i = rows[i]). Returns (nsel, d)."""
+    L = oracle_lib()
+    d = X.dim
+    ny = Y.nrows
+    Xa, Ya, V = _arrs(A, X, Y, f64)
+    dt = np.float64 if f64 else np.float32
+    sel = None if rows is None else np.ascontiguousarray(rows, dtype=np.int64)
+    nsel = A.nrows if sel is None else sel.size
+    Z = np.zeros(nsel * d, dtype=dt)
+    ptr = (lambda a: a.ctypes.data_as(PD)) if f64 else (lambda a: a.ctypes.data_as(PF))
+    fn = L.fmm_oracle_fused_mm_f64 if f64 else L.fmm_oracle_fused_mm_f32
+    rc = fn(A.nrows, A.ncols, A.row_ptr.ctypes.data_as(P64), A.col_idx.ctypes.data_as(P64),
+            None if V is None else ptr(V), d, ptr(Xa), ny, ptr(Ya), C.byref(_spec(spec)), lane_width,
+            threads or host_threads(), None if sel is None else sel.ctypes.data_as(P64),
+            0 if sel is None else sel.size, ptr(Z))
+    if rc != 0:
+        raise ValueError(f"oracle rejected the call (rc={rc})")
+    return Z.reshape(nsel, d)
+
+
+def oracle_part1d(row_ptr: np.ndarray, t: int) -> list:
+    b = np.zeros(t + 1, np.int64)
+    m = row_ptr.size - 1
+    if oracle_lib().fmm_oracle_part1d(m, np.ascontiguousarray(row_ptr, np.int64).ctypes.data_as(P64), t,
+                                      b.ctypes.data_as(P64)) != 0:
+        raise ValueError("part1d: worker count must be >= 1")
+    return [int(x) for x in b]
+
+
+class RefCall:
+    """The reference fusedmm::fused_mm prepared once (CsrMatrix/DenseMatrix
+    built), then run/timed repeatedly: the timed region is the fused_mm call
+    only, including its Z allocation and thread spawn, as in bench.hpp:98-111."""
+
+    def __init__(self, A, X, Y, spec, lane_width: int = 8, f64: bool = False):
+        L = ref_lib()
+        self.f64 = f64
+        Xa, Ya, V = _arrs(A, X, Y, f64)
+        self._keep = (Xa, Ya, V, A)
+        ptr = (lambda a: a.ctypes.data_as(PD)) if f64 else (lambda a: a.ctypes.data_as(PF))
+        prep = L.fmm_ref_prepare_f64 if f64 else L.fmm_ref_prepare_f32
+        self.m, self.d = A.nrows, X.dim
+        self.h = prep(A.nrows, A.ncols, A.row_ptr.ctypes.data_as(P64), A.col_idx.ctypes.data_as(P64),
+                      None if V is None else ptr(V), X.dim, ptr(Xa), Y.nrows, ptr(Ya),
+                      C.byref(_spec(spec)), lane_width)
+
+    def run(self, t: int | None = None, want_z: bool = True):
+        L = ref_lib()
+        dt = np.float64 if self.f64 else np.float32
+        Z = np.zeros(self.m * self.d, dt) if want_z else None
+        secs = C.c_double()
+        fn = L.fmm_ref_run_f64 if self.f64 else L.fmm_ref_run_f32
+        zp = None if Z is None else (Z.ctypes.data_as(PD) if self.f64 else Z.ctypes.data_as(PF))
+        rc = fn(self.h, t or host_threads(), zp, C.byref(secs))
+        if rc != 0:
+            raise ValueError(f"reference fused_mm threw (rc={rc})")
+        return (None if Z is None else Z.reshape(self.m, self.d)), secs.value
+
+    def unfused(self) -> np.ndarray:
+        Z = np.zeros(self.m * self.d, np.float32)
+        if ref_lib().fmm_ref_unfused_f32(self.h, Z.ctypes.data_as(PF)) != 0:
+            raise ValueError("reference unfused pipeline threw")
+        return Z.reshape(self.m, self.d)
+
+    def close(self):
+        if self.h:
+            (ref_lib().fmm_ref_release_f64 if self.f64 else ref_lib().fmm_ref_release_f32)(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def ref_fused_mm(A, X, Y, spec, t: int = 1, lane_width: int = 8, f64: bool = False) -> np.ndarray:
+    rc = RefCall(A, X, Y, spec, lane_width, f64)
+    Z, _ = rc.run(t)
+    rc.close()
+    return Z
+
+
+def ref_part1d(row_ptr: np.ndarray, t: int) -> list:
+    b = np.zeros(t + 1, np.int64)
+    m = row_ptr.size - 1
+    if ref_lib().fmm_ref_part1d(m, np.ascontiguousarray(row_ptr, np.int64).ctypes.data_as(P64), t,
+                                b.ctypes.data_as(P64)) != 0:
+        raise ValueError("part1d: worker count must be >= 1")
+    return [int(x) for x in b]
+
+
+def ref_rmat(scale: int, edge_factor: int, seed: int, abc=(0.57, 0.19, 0.19)):
+    """rmat_generate (rmat.hpp:24-61) as (row_ptr, col, val)."""
+    L = ref_lib()
+    nnz = L.fmm_ref_rmat(scale, edge_factor, *abc, seed, None, None, None)
+    n = 1 << scale
+    rp = np.zeros(n + 1, np.int64)
+    cl = np.zeros(nnz, np.int64)
+    vl = np.zeros(nnz, np.float32)
+    L.fmm_ref_rmat(scale, edge_factor, *abc, seed, rp.ctypes.data_as(P64), cl.ctypes.data_as(P64),
+                   vl.ctypes.data_as(PF))
+    return rp, cl, vl
+
+
+def row_errors(Z_gpu: np.ndarray, Z_cpu: np.ndarray) -> np.ndarray:
+    """Per-row normwise relative error ||z_gpu - z_cpu|| / ||z_cpu||, rows
+    where both are zero count as 0."""
+    a = np.asarray(Z_gpu, np.float64)
+    b = np.asarray(Z_cpu, np.float64)
+    num = np.linalg.norm(a - b, axis=1)
+    den = np.linalg.norm(b, axis=1)
+    out = np.zeros_like(num)
+    nz = den > 0
+    out[nz] = num[nz] / den[nz]
+    out[(~nz) & (num > 0)] = np.inf
+    return out

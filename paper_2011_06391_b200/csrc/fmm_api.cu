@@ -1,0 +1,716 @@
+// fmm_api.cu — the C ABI of libfusedmm_cuda (include/fusedmm_cuda.h).
+//
+// Replaces the reference driver fusedmm::fused_mm (kernel.hpp:297-353): where
+// the reference validates dims (check_dims, kernel.hpp:269-282), plans a 1D
+// nnz-balanced partition (part1d, kernel.hpp:24-49) and spawns t std::thread
+// workers over it (kernel.hpp:335-345), this library uploads the CSR once,
+// partitions it with the same part1d rule across `ngpu` shards (one CUDA
+// stream each), and launches the row kernels of fmm_kernels.cuh per shard.
+#define FMM_AUX_KERNELS
+#include "fmm_kernels.cuh"
+#include "fmm_dispatch.cuh"
+#include "fmm_plan.h"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace {
+
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t cap = 0;
+};
+
+struct Shard {
+    int dev = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t ext = nullptr;
+    bool use_ext = false;  // ext may legitimately be the legacy NULL stream
+    DevBuf X, Y, Z, Xb, partial;
+    cudaEvent_t ev_start = nullptr, ev_k0 = nullptr, ev_k1 = nullptr, ev_end = nullptr,
+                ev_copy = nullptr;
+    cudaStream_t stream() const { return use_ext ? ext : own; }
+};
+
+}  // namespace
+
+struct fmm_ctx {
+    std::vector<Shard> shards;
+    std::string err;
+    std::mutex mu;
+};
+
+namespace {
+
+struct GShard {
+    int shard = 0;
+    int64_t row_begin = 0, row_end = 0, nnz = 0;
+    int64_t n_split_rows = 0, n_chunks = 0, n_slots = 0, nonempty = 0, max_degree = 0;
+    int64_t* row_ptr = nullptr;
+    int32_t* col = nullptr;
+    float* val = nullptr;
+    int32_t* order = nullptr;
+    int4* chunks = nullptr;
+    int4* split_rows = nullptr;
+};
+
+}  // namespace
+
+struct fmm_graph {
+    fmm_ctx* ctx = nullptr;
+    int64_t m = 0, n = 0, nnz = 0, row_begin = 0, row_end = 0;
+    int64_t max_col = -1;
+    bool has_values = false;
+    std::vector<GShard> shards;
+};
+
+namespace {
+
+fmm_status set_err(fmm_ctx* ctx, fmm_status st, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return st;
+}
+
+fmm_status cuda_err(fmm_ctx* ctx, cudaError_t e, const char* what) {
+    const fmm_status st = (e == cudaErrorMemoryAllocation) ? FMM_E_OOM : FMM_E_CUDA;
+    return set_err(ctx, st, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define FMM_CK(ctx, call)                                            \
+    do {                                                             \
+        cudaError_t e_ = (call);                                     \
+        if (e_ != cudaSuccess) return cuda_err((ctx), e_, #call);    \
+    } while (0)
+
+fmm_status ensure(fmm_ctx* ctx, const Shard& sh, DevBuf& b, size_t bytes) {
+    if (bytes <= b.cap) return FMM_OK;
+    FMM_CK(ctx, cudaSetDevice(sh.dev));
+    if (b.ptr) {
+        FMM_CK(ctx, cudaStreamSynchronize(sh.stream()));
+        FMM_CK(ctx, cudaFree(b.ptr));
+        b.ptr = nullptr;
+        b.cap = 0;
+    }
+    FMM_CK(ctx, cudaMalloc(&b.ptr, bytes));
+    b.cap = bytes;
+    return FMM_OK;
+}
+
+template <class T>
+fmm_status upload_vec(fmm_ctx* ctx, const std::vector<T>& v, T** dst) {
+    *dst = nullptr;
+    if (v.empty()) return FMM_OK;
+    FMM_CK(ctx, cudaMalloc(reinterpret_cast<void**>(dst), v.size() * sizeof(T)));
+    FMM_CK(ctx, cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return FMM_OK;
+}
+
+bool is_user(const fmm_opspec& s) {
+    return s.vop == FMM_VOP_USER || s.rop == FMM_ROP_USER || s.sop == FMM_SOP_USER ||
+           s.mop == FMM_MOP_USER || s.aop == FMM_AOP_USER;
+}
+
+bool valid_codes(const fmm_opspec& s) {
+    const bool v = s.vop >= FMM_VOP_ADD && s.vop <= FMM_VOP_USER;
+    const bool r = (s.rop >= FMM_ROP_NOOP && s.rop <= FMM_ROP_USER) || s.rop == FMM_ROP_SQNORM;
+    const bool so = (s.sop >= FMM_SOP_NOOP && s.sop <= FMM_SOP_USER) || s.sop == FMM_SOP_TDIST ||
+                    s.sop == FMM_SOP_SQK;
+    const bool mo = (s.mop >= FMM_MOP_MUL && s.mop <= FMM_MOP_USER) || s.mop == FMM_MOP_MUL_VOP;
+    const bool a = s.aop >= FMM_AOP_ASUM && s.aop <= FMM_AOP_USER;
+    return v && r && so && mo && a;
+}
+
+// ops.hpp:189-203 plus the two device-only patterns.
+int pattern_of(const fmm_opspec& s) {
+    if (is_user(s)) return FMM_PATTERN_GENERIC;
+    auto is = [&](int v, int r, int so, int mo, int a) {
+        return s.vop == v && s.rop == r && s.sop == so && s.mop == mo && s.aop == a;
+    };
+    if (is(FMM_VOP_MUL, FMM_ROP_RSUM, FMM_SOP_SIGMOID, FMM_MOP_MUL, FMM_AOP_ASUM))
+        return FMM_PATTERN_SIGMOID_EMBED;
+    if (is(FMM_VOP_SEL2ND, FMM_ROP_NOOP, FMM_SOP_NOOP, FMM_MOP_MUL, FMM_AOP_ASUM))
+        return FMM_PATTERN_SPMM_GCN;
+    if (is(FMM_VOP_ADD, FMM_ROP_NORM, FMM_SOP_SCAL, FMM_MOP_MUL, FMM_AOP_ASUM))
+        return FMM_PATTERN_FR_LAYOUT;
+    if (is(FMM_VOP_SUB, FMM_ROP_SQNORM, FMM_SOP_TDIST, FMM_MOP_MUL_VOP, FMM_AOP_ASUM))
+        return FMM_PATTERN_TDIST;
+    if (is(FMM_VOP_SUB, FMM_ROP_SQNORM, FMM_SOP_SQK, FMM_MOP_MUL_VOP, FMM_AOP_ASUM))
+        return FMM_PATTERN_FR_ATTRACT;
+    return FMM_PATTERN_GENERIC;
+}
+
+// Default numerics scheme per pattern: bit-exact where the reference order is
+// reproducible without serialising rows (configs 1 and 4).
+bool default_exact(int pattern, int64_t d) {
+    if (pattern == FMM_PATTERN_SPMM_GCN) return true;
+    if (pattern == FMM_PATTERN_FR_ATTRACT && d <= 4) return true;
+    return false;
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+bool launch_rows(const fmm::KParams& p, int pattern, int d, bool exact, bool a16, bool a8,
+                 cudaStream_t s) {
+    const bool vec = fmm::aligned_shape(d, a16, a8);
+    if (vec) {
+        switch (pattern) {
+            case FMM_PATTERN_SIGMOID_EMBED: return fmm::launch_sigmoid(p, d, exact, s);
+            case FMM_PATTERN_SPMM_GCN: return fmm::launch_gcn(p, d, exact, s);
+            case FMM_PATTERN_FR_LAYOUT: return fmm::launch_fr(p, d, exact, s);
+            case FMM_PATTERN_TDIST: return fmm::launch_tdist(p, d, exact, s);
+            case FMM_PATTERN_FR_ATTRACT: return fmm::launch_frattr(p, d, exact, s);
+            default: break;
+        }
+    }
+    return fmm::launch_generic(p, d, exact, vec, s);
+}
+
+// Launch the fused kernels of one shard: rows (+ chunks) then the combine.
+// Returns the number of kernels launched, or -1 if no instantiation fits.
+int launch_shard(const GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, bool exact,
+                 const float* X, int64_t row0, const float* Y, float* Z, float* partial,
+                 const float* val, cudaStream_t stream) {
+    fmm::KParams p{};
+    p.row_ptr = gs.row_ptr;
+    p.col = gs.col;
+    p.val = val;
+    p.X = X;
+    p.Y = Y;
+    p.Z = Z;
+    p.partial = partial;
+    p.row0 = row0;
+    p.chunk = fmm::kChunkEdges;
+    p.d = static_cast<int>(d);
+    p.vop = spec.vop; p.rop = spec.rop; p.sop = spec.sop; p.mop = spec.mop; p.aop = spec.aop;
+    p.alpha = spec.alpha;
+    p.k = spec.k;
+    const int64_t rows = gs.row_end - gs.row_begin;
+    const bool split = !exact && gs.n_chunks > 0;
+    if (split) {
+        p.chunks = gs.chunks;
+        p.n_chunk_items = gs.n_chunks;
+        p.order = gs.order + gs.n_split_rows;
+        p.n_row_items = rows - gs.n_split_rows;
+    } else {
+        p.chunks = nullptr;
+        p.n_chunk_items = 0;
+        p.order = gs.order;
+        p.n_row_items = rows;
+    }
+    if (p.n_chunk_items + p.n_row_items == 0) return 0;
+    const size_t a = static_cast<size_t>(d) * sizeof(float);
+    const bool a16 = (d % 4 == 0) && aligned(X, 16) && aligned(Y, 16) && aligned(Z, 16) &&
+                     (partial == nullptr || aligned(partial, 16)) && (a % 16 == 0);
+    const bool a8 = (d % 2 == 0) && aligned(X, 8) && aligned(Y, 8) && aligned(Z, 8) &&
+                    (partial == nullptr || aligned(partial, 8));
+    if (!launch_rows(p, pattern, static_cast<int>(d), exact, a16, a8, stream)) return -1;
+    int launches = 1;
+    if (split && gs.n_split_rows > 0) {
+        fmm::fmm_combine_kernel<<<static_cast<unsigned>(gs.n_split_rows), 256, 0, stream>>>(
+            gs.split_rows, partial, Z, static_cast<int>(d), spec.aop == FMM_AOP_AMAX ? 1 : 0);
+        ++launches;
+    }
+    return launches;
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) return 0.f;
+    return ms;
+}
+
+fmm_status check_spec(fmm_ctx* ctx, const fmm_opspec* spec, int64_t d) {
+    if (!spec) return set_err(ctx, FMM_E_INVAL, "fused_mm: spec is NULL");
+    if (!valid_codes(*spec)) return set_err(ctx, FMM_E_INVAL, "fused_mm: unknown op code");
+    if (is_user(*spec))
+        return set_err(ctx, FMM_E_UNSUPPORTED,
+                       "fused_mm: USER slot has no device kernel (no CPU fallback)");
+    if (d < 1) return set_err(ctx, FMM_E_INVAL, "fused_mm: d must be >= 1");
+    if (d > 1024) return set_err(ctx, FMM_E_UNSUPPORTED, "fused_mm: d > 1024 not supported");
+    return FMM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fmm_version(void) { return "libfusedmm_cuda 0.1 (sm_100a)"; }
+
+const char* fmm_status_string(fmm_status s) {
+    switch (s) {
+        case FMM_OK: return "ok";
+        case FMM_E_INVAL: return "invalid argument";
+        case FMM_E_UNSUPPORTED: return "unsupported";
+        case FMM_E_CUDA: return "cuda error";
+        case FMM_E_NCCL: return "nccl error";
+        case FMM_E_OOM: return "out of memory";
+        case FMM_E_LOGIC: return "logic error";
+    }
+    return "unknown status";
+}
+
+int fmm_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+fmm_status fmm_create(int ngpu, const int* devs, fmm_ctx** out) {
+    if (!out) return FMM_E_INVAL;
+    *out = nullptr;
+    if (ngpu < 1) return FMM_E_INVAL;  // kernel.hpp:303: t must be >= 1
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return FMM_E_CUDA;
+    fmm_ctx* ctx = new (std::nothrow) fmm_ctx();
+    if (!ctx) return FMM_E_OOM;
+    ctx->shards.resize(ngpu);
+    for (int i = 0; i < ngpu; ++i) {
+        const int dev = devs ? devs[i] : (i % ndev);
+        if (dev < 0 || dev >= ndev) {
+            delete ctx;
+            return FMM_E_INVAL;
+        }
+        Shard& sh = ctx->shards[i];
+        sh.dev = dev;
+        if (cudaSetDevice(dev) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&sh.own, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreate(&sh.ev_start) != cudaSuccess || cudaEventCreate(&sh.ev_k0) != cudaSuccess ||
+            cudaEventCreate(&sh.ev_k1) != cudaSuccess || cudaEventCreate(&sh.ev_end) != cudaSuccess ||
+            cudaEventCreateWithFlags(&sh.ev_copy, cudaEventDisableTiming) != cudaSuccess) {
+            fmm_destroy(ctx);
+            return FMM_E_CUDA;
+        }
+    }
+    // peer access between distinct devices (NVLink / NVSwitch)
+    for (int i = 0; i < ngpu; ++i)
+        for (int j = 0; j < ngpu; ++j) {
+            const int a = ctx->shards[i].dev, b = ctx->shards[j].dev;
+            if (a == b) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, a, b);
+            if (can) {
+                cudaSetDevice(a);
+                const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            }
+        }
+    *out = ctx;
+    return FMM_OK;
+}
+
+fmm_status fmm_destroy(fmm_ctx* ctx) {
+    if (!ctx) return FMM_E_INVAL;
+    for (Shard& sh : ctx->shards) {
+        cudaSetDevice(sh.dev);
+        if (sh.own) cudaStreamSynchronize(sh.own);
+        for (DevBuf* b : {&sh.X, &sh.Y, &sh.Z, &sh.Xb, &sh.partial})
+            if (b->ptr) cudaFree(b->ptr);
+        for (cudaEvent_t e : {sh.ev_start, sh.ev_k0, sh.ev_k1, sh.ev_end, sh.ev_copy})
+            if (e) cudaEventDestroy(e);
+        if (sh.own) cudaStreamDestroy(sh.own);
+    }
+    delete ctx;
+    return FMM_OK;
+}
+
+const char* fmm_last_error(const fmm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+fmm_status fmm_set_stream(fmm_ctx* ctx, int shard, void* stream) {
+    if (!ctx || shard < 0 || shard >= static_cast<int>(ctx->shards.size())) return FMM_E_INVAL;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->shards[shard].ext = static_cast<cudaStream_t>(stream);
+    ctx->shards[shard].use_ext = true;
+    return FMM_OK;
+}
+
+fmm_status fmm_reset_stream(fmm_ctx* ctx, int shard) {
+    if (!ctx || shard < 0 || shard >= static_cast<int>(ctx->shards.size())) return FMM_E_INVAL;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->shards[shard].ext = nullptr;
+    ctx->shards[shard].use_ext = false;
+    return FMM_OK;
+}
+
+fmm_status fmm_pattern_of(const fmm_opspec* spec, int32_t* pattern) {
+    if (!spec || !pattern) return FMM_E_INVAL;
+    *pattern = pattern_of(*spec);
+    return FMM_OK;
+}
+
+fmm_status fmm_part1d(int64_t m, const int64_t* row_ptr, int t, int64_t* boundaries) {
+    if (m < 0 || !row_ptr || !boundaries || t < 1) return FMM_E_INVAL;
+    try {
+        const auto b = fmm::part1d(m, row_ptr, t);
+        std::memcpy(boundaries, b.data(), b.size() * sizeof(int64_t));
+    } catch (const std::exception&) {
+        return FMM_E_INVAL;
+    }
+    return FMM_OK;
+}
+
+fmm_status fmm_graph_upload(fmm_ctx* ctx, int64_t m, int64_t n, const int64_t* row_ptr,
+                            const int64_t* col_idx, const float* values, int64_t row_begin,
+                            int64_t row_end, fmm_graph** out) {
+    if (!ctx || !out) return FMM_E_INVAL;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    *out = nullptr;
+    if (m < 0 || n < 0 || !row_ptr) return set_err(ctx, FMM_E_INVAL, "graph_upload: bad sizes");
+    if (n > INT32_MAX) return set_err(ctx, FMM_E_UNSUPPORTED, "graph_upload: n >= 2^31");
+    if (row_begin < 0 || row_end > m || row_begin > row_end)
+        return set_err(ctx, FMM_E_INVAL, "graph_upload: bad row range");
+    const std::string bad = fmm::validate_row_ptr(m, row_ptr);
+    if (!bad.empty()) return set_err(ctx, FMM_E_INVAL, "graph_upload: " + bad);
+    if (row_ptr[m] > 0 && !col_idx) return set_err(ctx, FMM_E_INVAL, "graph_upload: col_idx NULL");
+
+    fmm_graph* g = new (std::nothrow) fmm_graph();
+    if (!g) return FMM_E_OOM;
+    g->ctx = ctx;
+    g->m = m;
+    g->n = n;
+    g->row_begin = row_begin;
+    g->row_end = row_end;
+    g->nnz = row_ptr[row_end] - row_ptr[row_begin];
+    g->has_values = values != nullptr;
+
+    const int S = static_cast<int>(ctx->shards.size());
+    // part1d over the requested row range (kernel.hpp:24-49)
+    std::vector<int64_t> bounds;
+    try {
+        bounds = fmm::part1d(row_end - row_begin, row_ptr + row_begin, S);
+    } catch (const std::exception& e) {
+        delete g;
+        return set_err(ctx, FMM_E_INVAL, e.what());
+    }
+    g->shards.resize(S);
+    fmm_status st = FMM_OK;
+    for (int s = 0; s < S && st == FMM_OK; ++s) {
+        GShard& gs = g->shards[s];
+        const Shard& sh = ctx->shards[s];
+        gs.shard = s;
+        gs.row_begin = row_begin + bounds[s];
+        gs.row_end = row_begin + bounds[s + 1];
+        fmm::ShardPlan P;
+        try {
+            P = fmm::build_shard_plan(row_ptr, gs.row_begin, gs.row_end);
+        } catch (const std::exception& e) {
+            st = set_err(ctx, FMM_E_UNSUPPORTED, e.what());
+            break;
+        }
+        gs.nnz = P.nnz;
+        gs.n_split_rows = P.n_split_rows;
+        gs.n_chunks = static_cast<int64_t>(P.chunks.size());
+        gs.n_slots = P.n_slots;
+        gs.nonempty = P.nonempty_rows;
+        gs.max_degree = P.max_degree;
+        if (cudaSetDevice(sh.dev) != cudaSuccess) { st = set_err(ctx, FMM_E_CUDA, "cudaSetDevice"); break; }
+        if ((st = upload_vec(ctx, P.local_row_ptr, &gs.row_ptr)) != FMM_OK) break;
+        if ((st = upload_vec(ctx, P.order, &gs.order)) != FMM_OK) break;
+        static_assert(sizeof(fmm::Int4) == sizeof(int4), "int4 layout");
+        std::vector<int4> ch(P.chunks.size()), sr(P.split_rows.size());
+        std::memcpy(ch.data(), P.chunks.data(), ch.size() * sizeof(int4));
+        std::memcpy(sr.data(), P.split_rows.data(), sr.size() * sizeof(int4));
+        if ((st = upload_vec(ctx, ch, &gs.chunks)) != FMM_OK) break;
+        if ((st = upload_vec(ctx, sr, &gs.split_rows)) != FMM_OK) break;
+        if (gs.nnz > 0) {
+            // narrow + validate columns in staged slices
+            auto fail = [&](cudaError_t e, const char* w) { st = cuda_err(ctx, e, w); };
+            cudaError_t e;
+            if ((e = cudaMalloc(&gs.col, gs.nnz * sizeof(int32_t))) != cudaSuccess) { fail(e, "cudaMalloc col"); break; }
+            const int64_t stage = std::min<int64_t>(gs.nnz, int64_t(1) << 24);
+            int64_t* tmp = nullptr;
+            int* flags = nullptr;
+            if ((e = cudaMalloc(&tmp, stage * sizeof(int64_t))) != cudaSuccess) { fail(e, "cudaMalloc stage"); break; }
+            if ((e = cudaMalloc(&flags, 2 * sizeof(int))) != cudaSuccess) { cudaFree(tmp); fail(e, "cudaMalloc flags"); break; }
+            int init[2] = {0, -1};
+            cudaMemcpy(flags, init, sizeof(init), cudaMemcpyHostToDevice);
+            for (int64_t off = 0; off < gs.nnz && st == FMM_OK; off += stage) {
+                const int64_t cnt = std::min(stage, gs.nnz - off);
+                e = cudaMemcpy(tmp, col_idx + P.edge_begin + off, cnt * sizeof(int64_t), cudaMemcpyHostToDevice);
+                if (e != cudaSuccess) { fail(e, "cudaMemcpy cols"); break; }
+                const int blocks = static_cast<int>(std::min<int64_t>((cnt + 255) / 256, 148 * 16));
+                fmm::fmm_narrow_cols_kernel<<<blocks, 256>>>(tmp, gs.col + off, cnt, n, flags, flags + 1);
+                if ((e = cudaGetLastError()) != cudaSuccess) { fail(e, "narrow kernel"); break; }
+            }
+            int res[2] = {0, -1};
+            if (st == FMM_OK) {
+                if ((e = cudaMemcpy(res, flags, sizeof(res), cudaMemcpyDeviceToHost)) != cudaSuccess) fail(e, "cudaMemcpy flags");
+            }
+            cudaFree(tmp);
+            cudaFree(flags);
+            if (st != FMM_OK) break;
+            if (res[0]) { st = set_err(ctx, FMM_E_INVAL, "graph_upload: column index out of range"); break; }
+            g->max_col = std::max<int64_t>(g->max_col, res[1]);
+            if (values) {
+                if ((e = cudaMalloc(&gs.val, gs.nnz * sizeof(float))) != cudaSuccess) { fail(e, "cudaMalloc val"); break; }
+                if ((e = cudaMemcpy(gs.val, values + P.edge_begin, gs.nnz * sizeof(float), cudaMemcpyHostToDevice)) != cudaSuccess) { fail(e, "cudaMemcpy val"); break; }
+            }
+        }
+    }
+    if (st != FMM_OK) {
+        fmm_graph_free(g);
+        return st;
+    }
+    *out = g;
+    return FMM_OK;
+}
+
+fmm_status fmm_graph_free(fmm_graph* g) {
+    if (!g) return FMM_E_INVAL;
+    for (GShard& gs : g->shards) {
+        cudaSetDevice(g->ctx->shards[gs.shard].dev);
+        for (void* p : {static_cast<void*>(gs.row_ptr), static_cast<void*>(gs.col), static_cast<void*>(gs.val),
+                        static_cast<void*>(gs.order), static_cast<void*>(gs.chunks),
+                        static_cast<void*>(gs.split_rows)})
+            if (p) cudaFree(p);
+    }
+    delete g;
+    return FMM_OK;
+}
+
+fmm_status fmm_graph_get_info(const fmm_graph* g, fmm_graph_info* out) {
+    if (!g || !out) return FMM_E_INVAL;
+    fmm_graph_info I{};
+    I.m = g->m;
+    I.n = g->n;
+    I.nnz = g->nnz;
+    I.row_begin = g->row_begin;
+    I.row_end = g->row_end;
+    I.shards = static_cast<int32_t>(g->shards.size());
+    I.has_values = g->has_values ? 1 : 0;
+    for (const GShard& gs : g->shards) {
+        I.nonempty_rows += gs.nonempty;
+        I.max_degree = std::max(I.max_degree, gs.max_degree);
+        I.split_rows += gs.n_split_rows;
+        I.split_chunks += gs.n_chunks;
+    }
+    *out = I;
+    return FMM_OK;
+}
+
+fmm_status fmm_graph_shard_bounds(const fmm_graph* g, int64_t* bounds) {
+    if (!g || !bounds) return FMM_E_INVAL;
+    for (size_t s = 0; s < g->shards.size(); ++s) bounds[s] = g->shards[s].row_begin;
+    bounds[g->shards.size()] = g->row_end;
+    return FMM_OK;
+}
+
+fmm_status fmm_run(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec, int64_t d,
+                   const float* X, int64_t ny, const float* Y, float* Z, uint32_t flags,
+                   fmm_stats* stats) {
+    if (!ctx || !g || g->ctx != ctx) return FMM_E_INVAL;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    fmm_status st = check_spec(ctx, spec, d);
+    if (st != FMM_OK) return st;
+    const int64_t rows = g->row_end - g->row_begin;
+    if (ny < 0) return set_err(ctx, FMM_E_INVAL, "fused_mm: negative Y rows");
+    // kernel.hpp:278-281: Y must cover every referenced column
+    if (g->nnz > 0 && ny < g->max_col + 1) return set_err(ctx, FMM_E_INVAL, "fused_mm: Y has too few rows");
+    if (rows > 0 && (!X || !Z)) return set_err(ctx, FMM_E_INVAL, "fused_mm: NULL X or Z");
+    if (g->nnz > 0 && !Y) return set_err(ctx, FMM_E_INVAL, "fused_mm: NULL Y");
+    const bool dev_ptrs = (flags & FMM_DEVICE_PTRS) != 0;
+    const bool async = dev_ptrs && (flags & FMM_ASYNC) != 0;
+    if (dev_ptrs && ctx->shards.size() != 1)
+        return set_err(ctx, FMM_E_INVAL, "fused_mm: device pointers need a single-shard context");
+    const int pattern = pattern_of(*spec);
+    bool exact = default_exact(pattern, d);
+    if (flags & FMM_EXACT) exact = true;
+    if (flags & FMM_FAST) exact = false;
+    const size_t row_bytes = static_cast<size_t>(d) * sizeof(float);
+    const bool alias = (X == Y) && (ny == g->m);
+    int launches = 0;
+    size_t aux = 0;
+    const bool timed = stats != nullptr && !async;
+
+    for (size_t s = 0; s < g->shards.size(); ++s) {
+        const GShard& gs = g->shards[s];
+        Shard& sh = ctx->shards[gs.shard];
+        FMM_CK(ctx, cudaSetDevice(sh.dev));
+        cudaStream_t stream = sh.stream();
+        const int64_t srows = gs.row_end - gs.row_begin;
+        const float* xd;
+        const float* yd;
+        float* zd;
+        int64_t row0;
+        if (timed) FMM_CK(ctx, cudaEventRecord(sh.ev_start, stream));
+        if (dev_ptrs) {
+            xd = X;
+            yd = Y;
+            zd = Z + (gs.row_begin - g->row_begin) * d;
+            row0 = gs.row_begin;
+        } else {
+            if ((st = ensure(ctx, sh, sh.Y, std::max<size_t>(1, ny * row_bytes))) != FMM_OK) return st;
+            if (ny > 0)
+                FMM_CK(ctx, cudaMemcpyAsync(sh.Y.ptr, Y, ny * row_bytes, cudaMemcpyHostToDevice, stream));
+            yd = static_cast<const float*>(sh.Y.ptr);
+            if (alias) {
+                xd = yd;
+                row0 = gs.row_begin;
+            } else {
+                if ((st = ensure(ctx, sh, sh.X, std::max<size_t>(1, srows * row_bytes))) != FMM_OK) return st;
+                if (srows > 0)
+                    FMM_CK(ctx, cudaMemcpyAsync(sh.X.ptr, X + gs.row_begin * d, srows * row_bytes,
+                                                cudaMemcpyHostToDevice, stream));
+                xd = static_cast<const float*>(sh.X.ptr);
+                row0 = 0;
+            }
+            if ((st = ensure(ctx, sh, sh.Z, std::max<size_t>(1, srows * row_bytes))) != FMM_OK) return st;
+            zd = static_cast<float*>(sh.Z.ptr);
+        }
+        float* part = nullptr;
+        if (!exact && gs.n_slots > 0) {
+            const size_t pb = static_cast<size_t>(gs.n_slots) * row_bytes;
+            if ((st = ensure(ctx, sh, sh.partial, pb)) != FMM_OK) return st;
+            part = static_cast<float*>(sh.partial.ptr);
+            aux = std::max(aux, pb);
+        }
+        if (timed) FMM_CK(ctx, cudaEventRecord(sh.ev_k0, stream));
+        const int l = launch_shard(gs, *spec, pattern, d, exact, xd, row0, yd, zd, part, gs.val, stream);
+        if (l < 0) return set_err(ctx, FMM_E_UNSUPPORTED, "fused_mm: no kernel for this d / alignment");
+        launches += l;
+        FMM_CK(ctx, cudaGetLastError());
+        if (timed) FMM_CK(ctx, cudaEventRecord(sh.ev_k1, stream));
+        if (!dev_ptrs && srows > 0)
+            FMM_CK(ctx, cudaMemcpyAsync(Z + (gs.row_begin - g->row_begin) * d, zd, srows * row_bytes,
+                                        cudaMemcpyDeviceToHost, stream));
+        if (timed) FMM_CK(ctx, cudaEventRecord(sh.ev_end, stream));
+    }
+    float kms = 0.f, tms = 0.f;
+    if (!async) {
+        for (const GShard& gs : g->shards) {
+            Shard& sh = ctx->shards[gs.shard];
+            FMM_CK(ctx, cudaSetDevice(sh.dev));
+            FMM_CK(ctx, cudaStreamSynchronize(sh.stream()));
+            if (timed) {
+                kms = std::max(kms, elapsed(sh.ev_k0, sh.ev_k1));
+                tms = std::max(tms, elapsed(sh.ev_start, sh.ev_end));
+            }
+        }
+    }
+    if (stats) {
+        stats->aux_bytes = aux;
+        stats->threads = static_cast<int32_t>(g->shards.size());
+        stats->pattern = pattern;
+        stats->exact = exact ? 1 : 0;
+        stats->launches = launches;
+        stats->kernel_ms = kms;
+        stats->total_ms = tms;
+    }
+    (void)rows;
+    return FMM_OK;
+}
+
+fmm_status fmm_iterate(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec, int64_t d,
+                       float* X, int iters, uint32_t flags, fmm_stats* stats) {
+    if (!ctx || !g || g->ctx != ctx) return FMM_E_INVAL;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    fmm_status st = check_spec(ctx, spec, d);
+    if (st != FMM_OK) return st;
+    if (iters < 0) return set_err(ctx, FMM_E_INVAL, "iterate: iters must be >= 0");
+    if (g->m != g->n || g->row_begin != 0 || g->row_end != g->m)
+        return set_err(ctx, FMM_E_INVAL, "iterate: needs a square graph uploaded over all rows");
+    if (flags & FMM_DEVICE_PTRS) return set_err(ctx, FMM_E_INVAL, "iterate: host pointers only");
+    if (g->m > 0 && !X) return set_err(ctx, FMM_E_INVAL, "iterate: NULL X");
+    const int pattern = pattern_of(*spec);
+    bool exact = default_exact(pattern, d);
+    if (flags & FMM_EXACT) exact = true;
+    if (flags & FMM_FAST) exact = false;
+    const int64_t m = g->m;
+    const size_t row_bytes = static_cast<size_t>(d) * sizeof(float);
+    const size_t full = std::max<size_t>(1, m * row_bytes);
+    const int S = static_cast<int>(g->shards.size());
+    int launches = 0;
+    size_t aux = 0;
+    // buffers + upload of X0 into every shard's current buffer
+    for (int s = 0; s < S; ++s) {
+        Shard& sh = ctx->shards[g->shards[s].shard];
+        if ((st = ensure(ctx, sh, sh.Y, full)) != FMM_OK) return st;
+        if ((st = ensure(ctx, sh, sh.Xb, full)) != FMM_OK) return st;
+        const GShard& gs = g->shards[s];
+        if (!exact && gs.n_slots > 0) {
+            const size_t pb = static_cast<size_t>(gs.n_slots) * row_bytes;
+            if ((st = ensure(ctx, sh, sh.partial, pb)) != FMM_OK) return st;
+            aux = std::max(aux, pb);
+        }
+    }
+    for (int s = 0; s < S; ++s) {
+        Shard& sh = ctx->shards[g->shards[s].shard];
+        FMM_CK(ctx, cudaSetDevice(sh.dev));
+        FMM_CK(ctx, cudaEventRecord(sh.ev_start, sh.stream()));
+        if (m > 0) FMM_CK(ctx, cudaMemcpyAsync(sh.Y.ptr, X, m * row_bytes, cudaMemcpyHostToDevice, sh.stream()));
+        FMM_CK(ctx, cudaEventRecord(sh.ev_k0, sh.stream()));
+    }
+    int cur = 0;  // 0: Y holds the iterate, 1: Xb holds it
+    for (int it = 0; it < iters; ++it) {
+        for (int s = 0; s < S; ++s) {
+            const GShard& gs = g->shards[s];
+            Shard& sh = ctx->shards[gs.shard];
+            FMM_CK(ctx, cudaSetDevice(sh.dev));
+            if (it > 0)
+                for (int q = 0; q < S; ++q)
+                    if (q != s) FMM_CK(ctx, cudaStreamWaitEvent(sh.stream(), ctx->shards[g->shards[q].shard].ev_copy, 0));
+            float* xc = static_cast<float*>(cur == 0 ? sh.Y.ptr : sh.Xb.ptr);
+            float* xn = static_cast<float*>(cur == 0 ? sh.Xb.ptr : sh.Y.ptr);
+            const int l = launch_shard(gs, *spec, pattern, d, exact, xc, gs.row_begin, xc,
+                                       xn + gs.row_begin * d, static_cast<float*>(sh.partial.ptr),
+                                       gs.val, sh.stream());
+            if (l < 0) return set_err(ctx, FMM_E_UNSUPPORTED, "iterate: no kernel for this d / alignment");
+            launches += l;
+            FMM_CK(ctx, cudaGetLastError());
+        }
+        if (it + 1 < iters && S > 1) {
+            // exchange: every shard pushes its fresh Z slice into every peer's next buffer
+            for (int s = 0; s < S; ++s) {
+                const GShard& gs = g->shards[s];
+                Shard& sh = ctx->shards[gs.shard];
+                FMM_CK(ctx, cudaSetDevice(sh.dev));
+                const float* src = static_cast<const float*>(cur == 0 ? sh.Xb.ptr : sh.Y.ptr) + gs.row_begin * d;
+                const size_t bytes = (gs.row_end - gs.row_begin) * row_bytes;
+                for (int q = 0; q < S && bytes > 0; ++q) {
+                    if (q == s) continue;
+                    Shard& sq = ctx->shards[g->shards[q].shard];
+                    float* dst = static_cast<float*>(cur == 0 ? sq.Xb.ptr : sq.Y.ptr) + gs.row_begin * d;
+                    FMM_CK(ctx, cudaMemcpyPeerAsync(dst, sq.dev, src, sh.dev, bytes, sh.stream()));
+                }
+                FMM_CK(ctx, cudaEventRecord(sh.ev_copy, sh.stream()));
+            }
+        }
+        cur ^= 1;
+    }
+    for (int s = 0; s < S; ++s) {
+        const GShard& gs = g->shards[s];
+        Shard& sh = ctx->shards[gs.shard];
+        FMM_CK(ctx, cudaSetDevice(sh.dev));
+        FMM_CK(ctx, cudaEventRecord(sh.ev_k1, sh.stream()));
+        const float* src = static_cast<const float*>(cur == 0 ? sh.Y.ptr : sh.Xb.ptr) + gs.row_begin * d;
+        const size_t bytes = (gs.row_end - gs.row_begin) * row_bytes;
+        if (bytes > 0)
+            FMM_CK(ctx, cudaMemcpyAsync(X + gs.row_begin * d, src, bytes, cudaMemcpyDeviceToHost, sh.stream()));
+        FMM_CK(ctx, cudaEventRecord(sh.ev_end, sh.stream()));
+    }
+    float kms = 0.f, tms = 0.f;
+    for (int s = 0; s < S; ++s) {
+        Shard& sh = ctx->shards[g->shards[s].shard];
+        FMM_CK(ctx, cudaSetDevice(sh.dev));
+        FMM_CK(ctx, cudaStreamSynchronize(sh.stream()));
+        kms = std::max(kms, elapsed(sh.ev_k0, sh.ev_k1));
+        tms = std::max(tms, elapsed(sh.ev_start, sh.ev_end));
+    }
+    if (stats) {
+        stats->aux_bytes = aux;
+        stats->threads = S;
+        stats->pattern = pattern;
+        stats->exact = exact ? 1 : 0;
+        stats->launches = launches;
+        stats->kernel_ms = kms;
+        stats->total_ms = tms;
+    }
+    return FMM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,220 @@
+// fmm_gen.cpp — seeded synthetic inputs for the five BASELINE.json configs
+// (host C++, exported as a plain C ABI in libfmm_gen.so).
+//
+// These are input generators, not part of the fused path. They restate the
+// published R-MAT recursive-quadrant algorithm with the reference's RNG
+// conventions — std::mt19937_64(seed), u01 = (rng() >> 11) * 2^-53 and the
+// quadrant descent of rmat.hpp:32-58 — and the post-processing BASELINE.json
+// asks for (self-loops dropped, symmetrised, deduplicated, columns sorted).
+// The recipes are written out in SURVEY.md §8(d) and DESIGN.md.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <random>
+#include <vector>
+
+namespace {
+
+struct U01 {
+    std::mt19937_64 rng;
+    explicit U01(uint64_t seed) : rng(seed) {}
+    double operator()() { return static_cast<double>(rng() >> 11) * 0x1.0p-53; }
+};
+
+// LSD radix sort of 64-bit keys on the low `bits` bits, 16 bits per pass.
+void radix_sort(std::vector<uint64_t>& keys, int bits) {
+    std::vector<uint64_t> tmp(keys.size());
+    for (int shift = 0; shift < bits; shift += 16) {
+        std::vector<size_t> cnt(65537, 0);
+        for (uint64_t k : keys) ++cnt[((k >> shift) & 0xffff) + 1];
+        for (int i = 0; i < 65536; ++i) cnt[i + 1] += cnt[i];
+        for (uint64_t k : keys) tmp[cnt[(k >> shift) & 0xffff]++] = k;
+        keys.swap(tmp);
+    }
+}
+
+// keys = (row << 32) | col, sorted -> unique -> CSR
+void keys_to_csr(std::vector<uint64_t>& keys, int64_t m, int key_bits, int64_t** row_ptr,
+                 int64_t** col, int64_t* nnz) {
+    radix_sort(keys, key_bits);
+    keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+    *nnz = static_cast<int64_t>(keys.size());
+    *row_ptr = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (m + 1)));
+    *col = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * std::max<size_t>(1, keys.size())));
+    std::memset(*row_ptr, 0, sizeof(int64_t) * (m + 1));
+    for (size_t i = 0; i < keys.size(); ++i) {
+        (*row_ptr)[(keys[i] >> 32) + 1]++;
+        (*col)[i] = static_cast<int64_t>(keys[i] & 0xffffffffu);
+    }
+    for (int64_t r = 0; r < m; ++r) (*row_ptr)[r + 1] += (*row_ptr)[r];
+}
+
+int bits_for(int64_t m) {
+    int b = 0;
+    while ((int64_t(1) << b) < m) ++b;
+    return b;
+}
+
+}  // namespace
+
+extern "C" {
+
+void fmmgen_free(void* p) { std::free(p); }
+
+// Config 1: n rows, each with exactly k distinct out-neighbours drawn as
+// floor(u01*n) until k are distinct (self allowed), sorted ascending; then
+// a_uv = u01 drawn in sorted order. X (n x d, optional) continues the same
+// stream as U(-1,1): x = -1 + 2*u01.
+int fmmgen_er_fixed(int64_t n, int k, uint64_t seed, int64_t* row_ptr, int64_t* col, float* val,
+                    float* X, int64_t d) {
+    if (n < 1 || k < 0 || k > n) return 1;
+    U01 u(seed);
+    std::vector<int64_t> pick;
+    pick.reserve(k);
+    row_ptr[0] = 0;
+    for (int64_t r = 0; r < n; ++r) {
+        pick.clear();
+        while (static_cast<int>(pick.size()) < k) {
+            const int64_t v = static_cast<int64_t>(u() * static_cast<double>(n));
+            if (std::find(pick.begin(), pick.end(), v) == pick.end()) pick.push_back(v);
+        }
+        std::sort(pick.begin(), pick.end());
+        for (int i = 0; i < k; ++i) {
+            col[r * k + i] = pick[i];
+            val[r * k + i] = static_cast<float>(u());
+        }
+        row_ptr[r + 1] = (r + 1) * k;
+    }
+    if (X)
+        for (int64_t i = 0; i < n * d; ++i) X[i] = static_cast<float>(-1.0 + 2.0 * u());
+    return 0;
+}
+
+// Configs 2, 3, 5: the R-MAT insertion stream of rmat.hpp:24-61 (scale,
+// edge_factor * 2^scale insertions, quadrant probabilities a, b, c, 1-a-b-c),
+// then self-loops dropped, every (u,v) inserted as (u,v) and (v,u), sorted and
+// deduplicated. Arrays are malloc'd; release with fmmgen_free.
+int fmmgen_rmat_sym(int scale, int edge_factor, double a, double b, double c, uint64_t seed,
+                    int64_t** row_ptr, int64_t** col, int64_t* nnz) {
+    if (scale < 1 || scale > 30 || edge_factor < 0) return 1;
+    const int64_t nverts = int64_t(1) << scale;
+    const int64_t nedges = static_cast<int64_t>(edge_factor) * nverts;
+    U01 u(seed);
+    const double ab = a + b, abc = a + b + c;
+    std::vector<uint64_t> keys;
+    keys.reserve(static_cast<size_t>(2 * nedges));
+    for (int64_t e = 0; e < nedges; ++e) {
+        uint64_t row = 0, cl = 0;
+        for (int level = 0; level < scale; ++level) {
+            const double x = u();
+            row <<= 1;
+            cl <<= 1;
+            if (x < a) {
+            } else if (x < ab) {
+                cl |= 1;
+            } else if (x < abc) {
+                row |= 1;
+            } else {
+                row |= 1;
+                cl |= 1;
+            }
+        }
+        if (row == cl) continue;
+        keys.push_back((row << 32) | cl);
+        keys.push_back((cl << 32) | row);
+    }
+    keys_to_csr(keys, nverts, 32 + scale, row_ptr, col, nnz);
+    return 0;
+}
+
+// The raw (un-postprocessed) R-MAT insertion stream as COO, for cross-checks
+// against the reference generator. rows/cols must hold edge_factor*2^scale.
+int fmmgen_rmat_stream(int scale, int edge_factor, double a, double b, double c, uint64_t seed,
+                       int64_t* rows, int64_t* cols) {
+    if (scale < 1 || scale > 30) return 1;
+    const int64_t nedges = static_cast<int64_t>(edge_factor) << scale;
+    U01 u(seed);
+    const double ab = a + b, abc = a + b + c;
+    for (int64_t e = 0; e < nedges; ++e) {
+        int64_t row = 0, cl = 0;
+        for (int level = 0; level < scale; ++level) {
+            const double x = u();
+            row <<= 1;
+            cl <<= 1;
+            if (x < a) {
+            } else if (x < ab) {
+                cl |= 1;
+            } else if (x < abc) {
+                row |= 1;
+            } else {
+                row |= 1;
+                cl |= 1;
+            }
+        }
+        rows[e] = row;
+        cols[e] = cl;
+    }
+    return 0;
+}
+
+// Config 4: side x side 4-neighbour lattice (v = r*side + c; right and down
+// edges) plus, for every v in order, one shortcut w = floor(u01*n) (dropped
+// when w == v); symmetrised, deduplicated, sorted. X (n x 2, optional)
+// continues the stream: x_v = (c + 0.01*N, r + 0.01*N), normals by
+// Box-Muller on two u01 draws (both outputs used).
+int fmmgen_lattice(int64_t side, uint64_t seed, int64_t** row_ptr, int64_t** col, int64_t* nnz,
+                   float* X) {
+    if (side < 1 || side > 46340) return 1;
+    const int64_t n = side * side;
+    U01 u(seed);
+    std::vector<uint64_t> keys;
+    keys.reserve(static_cast<size_t>(6 * n));
+    auto add = [&](uint64_t p, uint64_t q) {
+        keys.push_back((p << 32) | q);
+        keys.push_back((q << 32) | p);
+    };
+    for (int64_t r = 0; r < side; ++r)
+        for (int64_t c = 0; c < side; ++c) {
+            const uint64_t v = static_cast<uint64_t>(r * side + c);
+            if (c + 1 < side) add(v, v + 1);
+            if (r + 1 < side) add(v, v + static_cast<uint64_t>(side));
+        }
+    for (int64_t v = 0; v < n; ++v) {
+        const int64_t w = static_cast<int64_t>(u() * static_cast<double>(n));
+        if (w != v) add(static_cast<uint64_t>(v), static_cast<uint64_t>(w));
+    }
+    keys_to_csr(keys, n, 32 + bits_for(n), row_ptr, col, nnz);
+    if (X) {
+        const double two_pi = 6.283185307179586476925286766559;
+        for (int64_t v = 0; v < n; ++v) {
+            const double u1 = u(), u2 = u();
+            const double rad = std::sqrt(-2.0 * std::log(1.0 - u1));
+            const double n0 = rad * std::cos(two_pi * u2), n1 = rad * std::sin(two_pi * u2);
+            X[2 * v + 0] = static_cast<float>(static_cast<double>(v % side) + 0.01 * n0);
+            X[2 * v + 1] = static_cast<float>(static_cast<double>(v / side) + 0.01 * n1);
+        }
+    }
+    return 0;
+}
+
+// X[i] = scale * N(0,1), Box-Muller pairs from a fresh mt19937_64(seed).
+void fmmgen_normal_fill(float* X, int64_t count, double scale, uint64_t seed) {
+    U01 u(seed);
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int64_t i = 0; i < count; i += 2) {
+        const double u1 = u(), u2 = u();
+        const double rad = std::sqrt(-2.0 * std::log(1.0 - u1));
+        X[i] = static_cast<float>(scale * rad * std::cos(two_pi * u2));
+        if (i + 1 < count) X[i + 1] = static_cast<float>(scale * rad * std::sin(two_pi * u2));
+    }
+}
+
+// X[i] = lo + (hi-lo)*u01 from a fresh mt19937_64(seed).
+void fmmgen_uniform_fill(float* X, int64_t count, double lo, double hi, uint64_t seed) {
+    U01 u(seed);
+    for (int64_t i = 0; i < count; ++i) X[i] = static_cast<float>(lo + (hi - lo) * u());
+}
+
+}  // extern "C"

@@ -1,0 +1,3 @@
+// Row-kernel instantiations for the OpsFrAttr pattern (see fmm_kernels.cuh).
+#include "fmm_dispatch.cuh"
+FMM_DEFINE_STATIC_LAUNCH(launch_frattr, OpsFrAttr)

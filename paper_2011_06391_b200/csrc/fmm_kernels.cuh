@@ -1,0 +1,498 @@
+// fmm_kernels.cuh — sm_100a FusedMM row kernels.
+//
+// One lane group of LPR lanes owns one work item (a whole CSR row, or a
+// fixed-size chunk of a heavy row). The group keeps x_u and the z_u
+// accumulator in registers, streams the row's column indices with one
+// coalesced load per lane and broadcasts them with shuffles, gathers the
+// neighbour rows y_v with 128-bit loads (UNROLL rows in flight per group),
+// reduces the per-edge VOP output across the group with xor-butterflies, and
+// stores z_u once. This is the device restatement of
+//   fusedmm::update_u            kernel.hpp:81-107  (generic five-slot loop)
+//   detail::row_sigmoid_embed    kernel.hpp:118-143
+//   detail::row_spmm_gcn         kernel.hpp:145-158
+//   detail::row_fr_layout        kernel.hpp:160-190
+// with the per-slot arithmetic of ops.hpp:53-187.
+//
+// Numerics schemes (template flag EXACT):
+//   EXACT=true  — no FMA contraction (__fmul_rn/__fadd_rn, the reference is
+//                 built with -ffp-contract=off, CMakeLists.txt:25), neighbour
+//                 order strictly sequential per row (rows never split), lane-
+//                 local reductions in element order. Bit-identical to the
+//                 reference whenever the d-reduction is lane-local (LPR == 1)
+//                 or absent (SPMM_GCN) — configs 1 and 4.
+//   EXACT=false — FMA, heavy rows split into chunks combined in fixed chunk
+//                 order (deterministic, independent of the shard count).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fusedmm_cuda.h"
+
+namespace fmm {
+
+struct KParams {
+    const int64_t* row_ptr;  // shard-local, rebased to 0, rows+1 entries
+    const int32_t* col;      // shard-local edge columns (narrowed to int32)
+    const float* val;        // a_uv per edge, or nullptr (all ones)
+    const float* X;          // x_u = X + (row0 + r) * d
+    const float* Y;          // y_v = Y + v * d
+    float* Z;                // z_r = Z + r * d   (r shard-local)
+    float* partial;          // chunk partial rows: partial + slot * d
+    const int32_t* order;    // row items (shard-local rows)
+    const int4* chunks;      // chunk items {row, k, slot, 0}
+    int64_t n_chunk_items;
+    int64_t n_row_items;
+    int64_t row0;
+    int chunk;               // edges per chunk (fast scheme)
+    int d;
+    // dynamic op codes (used by DOps only)
+    int vop, rop, sop, mop, aop;
+    float alpha, k;
+};
+
+// ---------------------------------------------------------------- op kinds
+template <int V, int R, int S, int M, int A>
+struct SOps {
+    __device__ __forceinline__ int vop() const { return V; }
+    __device__ __forceinline__ int rop() const { return R; }
+    __device__ __forceinline__ int sop() const { return S; }
+    __device__ __forceinline__ int mop() const { return M; }
+    __device__ __forceinline__ int aop() const { return A; }
+};
+struct DOps {
+    int v, r, s, m, a;
+    __device__ __forceinline__ int vop() const { return v; }
+    __device__ __forceinline__ int rop() const { return r; }
+    __device__ __forceinline__ int sop() const { return s; }
+    __device__ __forceinline__ int mop() const { return m; }
+    __device__ __forceinline__ int aop() const { return a; }
+};
+
+using OpsSigmoid = SOps<FMM_VOP_MUL, FMM_ROP_RSUM, FMM_SOP_SIGMOID, FMM_MOP_MUL, FMM_AOP_ASUM>;
+using OpsGcn = SOps<FMM_VOP_SEL2ND, FMM_ROP_NOOP, FMM_SOP_NOOP, FMM_MOP_MUL, FMM_AOP_ASUM>;
+using OpsFr = SOps<FMM_VOP_ADD, FMM_ROP_NORM, FMM_SOP_SCAL, FMM_MOP_MUL, FMM_AOP_ASUM>;
+using OpsTdist = SOps<FMM_VOP_SUB, FMM_ROP_SQNORM, FMM_SOP_TDIST, FMM_MOP_MUL_VOP, FMM_AOP_ASUM>;
+using OpsFrAttr = SOps<FMM_VOP_SUB, FMM_ROP_SQNORM, FMM_SOP_SQK, FMM_MOP_MUL_VOP, FMM_AOP_ASUM>;
+
+// ------------------------------------------------------------- arithmetic
+template <bool EXACT>
+__device__ __forceinline__ float fmul(float a, float b) {
+    if constexpr (EXACT) return __fmul_rn(a, b);
+    else return a * b;
+}
+template <bool EXACT>
+__device__ __forceinline__ float fadd(float a, float b) {
+    if constexpr (EXACT) return __fadd_rn(a, b);
+    else return a + b;
+}
+template <bool EXACT>
+__device__ __forceinline__ float fsub(float a, float b) {
+    if constexpr (EXACT) return __fsub_rn(a, b);
+    else return a - b;
+}
+// acc + a*b : separate roundings when EXACT (reference: acc += a*b without FMA)
+template <bool EXACT>
+__device__ __forceinline__ float fmac(float acc, float a, float b) {
+    if constexpr (EXACT) return __fadd_rn(acc, __fmul_rn(a, b));
+    else return fmaf(a, b, acc);
+}
+
+// ops.hpp:58-80
+template <bool EXACT, class Ops>
+__device__ __forceinline__ float vop_apply(const Ops& ops, float x, float y) {
+    switch (ops.vop()) {
+        case FMM_VOP_ADD: return fadd<EXACT>(x, y);
+        case FMM_VOP_MUL: return fmul<EXACT>(x, y);
+        case FMM_VOP_SEL2ND: return y;
+        default: return fsub<EXACT>(x, y);  // FMM_VOP_SUB
+    }
+}
+
+__device__ __forceinline__ bool rop_is_product(int rop) { return rop == FMM_ROP_RMUL; }
+
+// lane-local step of ops.hpp:82-106 (RSUM / RMUL / NORM / SQNORM)
+template <bool EXACT, class Ops>
+__device__ __forceinline__ float rop_step(const Ops& ops, float acc, float t) {
+    switch (ops.rop()) {
+        case FMM_ROP_RMUL: return fmul<EXACT>(acc, t);
+        case FMM_ROP_NORM:
+        case FMM_ROP_SQNORM: return fmac<EXACT>(acc, t, t);
+        default: return fadd<EXACT>(acc, t);  // RSUM
+    }
+}
+
+// Fused "t = vop(x,y); acc = rop_step(acc, t)" — lets the fast scheme emit one
+// FMA per element for the MUL/RSUM dot product.
+template <bool EXACT, class Ops>
+__device__ __forceinline__ float vop_rop_step(const Ops& ops, float acc, float x, float y) {
+    if (ops.vop() == FMM_VOP_MUL && ops.rop() == FMM_ROP_RSUM) return fmac<EXACT>(acc, x, y);
+    return rop_step<EXACT>(ops, acc, vop_apply<EXACT>(ops, x, y));
+}
+
+// ops.hpp:53-56, 108-121 plus the device extensions TDIST / SQK
+template <class Ops>
+__device__ __forceinline__ float sop_apply(const Ops& ops, float s, float alpha, float k) {
+    switch (ops.sop()) {
+        case FMM_SOP_SIGMOID: return 1.0f / (1.0f + expf(-s));
+        case FMM_SOP_SCAL: return __fmul_rn(alpha, s);
+        case FMM_SOP_TDIST: return 1.0f / (1.0f + s);
+        case FMM_SOP_SQK: return __fdiv_rn(s, k);
+        default: return s;  // NOOP
+    }
+}
+
+// ops.hpp:166-182 (AMAX mirrors std::max(acc, w) == (acc < w ? w : acc))
+template <bool EXACT, class Ops>
+__device__ __forceinline__ float aop_apply(const Ops& ops, float acc, float w) {
+    if (ops.aop() == FMM_AOP_AMAX) return (acc < w) ? w : acc;
+    return fadd<EXACT>(acc, w);
+}
+
+template <class Ops>
+__device__ __forceinline__ float aop_identity(const Ops& ops) {
+    return ops.aop() == FMM_AOP_AMAX ? -__int_as_float(0x7f800000) : 0.0f;
+}
+
+// ------------------------------------------------------------ memory ops
+template <int VEC> struct VecT;
+template <> struct VecT<4> { using T = float4; };
+template <> struct VecT<2> { using T = float2; };
+template <> struct VecT<1> { using T = float; };
+
+template <int VEC>
+__device__ __forceinline__ void load_vec(float* dst, const float* src) {
+    if constexpr (VEC == 4) {
+        float4 v = __ldg(reinterpret_cast<const float4*>(src));
+        dst[0] = v.x; dst[1] = v.y; dst[2] = v.z; dst[3] = v.w;
+    } else if constexpr (VEC == 2) {
+        float2 v = __ldg(reinterpret_cast<const float2*>(src));
+        dst[0] = v.x; dst[1] = v.y;
+    } else {
+        dst[0] = __ldg(src);
+    }
+}
+template <int VEC>
+__device__ __forceinline__ void store_vec(float* dst, const float* src) {
+    if constexpr (VEC == 4) {
+        *reinterpret_cast<float4*>(dst) = make_float4(src[0], src[1], src[2], src[3]);
+    } else if constexpr (VEC == 2) {
+        *reinterpret_cast<float2*>(dst) = make_float2(src[0], src[1]);
+    } else {
+        dst[0] = src[0];
+    }
+}
+__device__ __forceinline__ int ld_stream_i32(const int32_t* p) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_stream_f32(const float* p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+
+// xor-butterfly over the LPR lanes of a group; every lane ends with the same
+// bits (a+b == b+a in IEEE arithmetic), so all lanes agree on h.
+template <int LPR>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+    for (int off = LPR / 2; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+template <int LPR>
+__device__ __forceinline__ float group_prod(float v) {
+#pragma unroll
+    for (int off = LPR / 2; off > 0; off >>= 1) v *= __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+// --------------------------------------------------------------- the kernel
+// Template shape: lane group of LPR lanes, each lane holding NV vectors of
+// VEC floats: element j = (i*LPR + lane)*VEC + c. MASKED kernels (VEC == 1)
+// serve any d <= 32*NV with lanes past d idle.
+template <class Ops, int LPR, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED>
+__global__ void __launch_bounds__(256)
+fmm_rows_kernel(const KParams p, const Ops ops) {
+    constexpr int NE = NV * VEC;
+    constexpr int B = (LPR > UNROLL) ? LPR : UNROLL;  // edges per batch
+    constexpr int KPL = B / LPR;                       // column slots per lane
+    static_assert(B % LPR == 0 && B % UNROLL == 0, "batch shape");
+
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & (LPR - 1);
+    const int gbase = lane & ~(LPR - 1);
+    const int64_t gid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / LPR;
+    const int64_t total = p.n_chunk_items + p.n_row_items;
+    const bool active = gid < total;
+    if (__all_sync(0xffffffffu, !active)) return;
+
+    const int d = MASKED ? p.d : LPR * VEC * NV;
+    const bool scalar_msg = ops.rop() != FMM_ROP_NOOP;
+    const bool need_x = ops.vop() != FMM_VOP_SEL2ND;
+    const bool has_val = p.val != nullptr;
+
+    int64_t r = 0, e0 = 0, e1 = 0;
+    float* out = nullptr;
+    if (active) {
+        if (gid < p.n_chunk_items) {
+            const int4 c = p.chunks[gid];
+            r = c.x;
+            const int64_t rb = p.row_ptr[r], re = p.row_ptr[r + 1];
+            e0 = rb + static_cast<int64_t>(c.y) * p.chunk;
+            e1 = min(e0 + static_cast<int64_t>(p.chunk), re);
+            out = p.partial + static_cast<int64_t>(c.z) * d;
+        } else {
+            r = p.order[gid - p.n_chunk_items];
+            e0 = p.row_ptr[r];
+            e1 = p.row_ptr[r + 1];
+            out = p.Z + r * d;
+        }
+    }
+    const int n = static_cast<int>(e1 - e0);
+    const int nmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(n)));
+
+    // x_u and z_u in registers
+    float x[NE], z[NE];
+    const float ident = aop_identity(ops);
+#pragma unroll
+    for (int i = 0; i < NE; ++i) { x[i] = 0.0f; z[i] = ident; }
+    bool elem_ok[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) elem_ok[i] = !MASKED || ((i * LPR + gl) * VEC < d);
+    if (active && need_x) {
+        const float* xr = p.X + (p.row0 + r) * d;
+#pragma unroll
+        for (int i = 0; i < NV; ++i)
+            if (elem_ok[i]) load_vec<VEC>(&x[i * VEC], xr + (i * LPR + gl) * VEC);
+    }
+
+    for (int base = 0; base < nmax; base += B) {
+        // column indices (and a_uv) of this batch: edge b lives in lane b % LPR, slot b / LPR
+        int cidx[KPL];
+        float aval[KPL];
+#pragma unroll
+        for (int q = 0; q < KPL; ++q) {
+            const int eb = base + q * LPR + gl;
+            cidx[q] = 0;
+            aval[q] = 1.0f;
+            if (eb < n) {
+                cidx[q] = ld_stream_i32(p.col + e0 + eb);
+                if (has_val) aval[q] = ld_stream_f32(p.val + e0 + eb);
+            }
+        }
+        const int cnt = min(B, nmax - base);  // warp-uniform
+        // B == UNROLL: one sub-batch (unrolled, static slot indices).
+        // B > UNROLL only when LPR > UNROLL, i.e. one column slot per lane.
+#pragma unroll 1
+        for (int u0 = 0; u0 < B; u0 += UNROLL) {
+            if (u0 >= cnt) break;
+            float y[UNROLL][NE];
+            float a[UNROLL];
+            bool ok[UNROLL];
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) {
+                const int b = u0 + u;
+                const int v = __shfl_sync(0xffffffffu, cidx[KPL == 1 ? 0 : b / LPR], gbase + (b % LPR));
+                a[u] = has_val ? __shfl_sync(0xffffffffu, aval[KPL == 1 ? 0 : b / LPR], gbase + (b % LPR)) : 1.0f;
+                ok[u] = (base + b) < n;
+                const float* yr = p.Y + static_cast<int64_t>(v) * d;
+#pragma unroll
+                for (int i = 0; i < NV; ++i) {
+                    if (ok[u] && elem_ok[i]) {
+                        load_vec<VEC>(&y[u][i * VEC], yr + (i * LPR + gl) * VEC);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < VEC; ++c) y[u][i * VEC + c] = 0.0f;
+                    }
+                }
+            }
+            if (scalar_msg) {
+                // ROP per edge: lane-local partial, then butterfly across the group
+                const bool prod = rop_is_product(ops.rop());
+                float s[UNROLL];
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u) {
+                    float acc = prod ? 1.0f : 0.0f;
+#pragma unroll
+                    for (int i = 0; i < NV; ++i) {
+                        if (!elem_ok[i]) continue;
+#pragma unroll
+                        for (int c = 0; c < VEC; ++c)
+                            acc = vop_rop_step<EXACT>(ops, acc, x[i * VEC + c], y[u][i * VEC + c]);
+                    }
+                    s[u] = acc;
+                }
+                if (LPR > 1) {
+#pragma unroll
+                    for (int u = 0; u < UNROLL; ++u)
+                        s[u] = prod ? group_prod<LPR>(s[u]) : group_sum<LPR>(s[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u) {
+                    float sv = s[u];
+                    if (ops.rop() == FMM_ROP_NORM) sv = sqrtf(sv);
+                    const float h = sop_apply(ops, sv, p.alpha, p.k);
+                    if (!ok[u]) continue;
+#pragma unroll
+                    for (int e = 0; e < NE; ++e) {
+                        float w;
+                        if (ops.mop() == FMM_MOP_SEL2ND) {
+                            w = y[u][e];
+                        } else if (ops.mop() == FMM_MOP_MUL_VOP) {
+                            const float t = vop_apply<EXACT>(ops, x[e], y[u][e]);
+                            w = fmul<EXACT>(a[u], fmul<EXACT>(h, t));
+                        } else {  // MUL: h * y_v, a_uv ignored (ops.hpp:131-137)
+                            if (ops.aop() == FMM_AOP_ASUM) {
+                                z[e] = fmac<EXACT>(z[e], h, y[u][e]);
+                                continue;
+                            }
+                            w = fmul<EXACT>(h, y[u][e]);
+                        }
+                        z[e] = aop_apply<EXACT>(ops, z[e], w);
+                    }
+                }
+            } else {
+                // vector message: SOP elementwise, MOP with a_uv (ops.hpp:123-127, 150-156)
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u) {
+                    if (!ok[u]) continue;
+#pragma unroll
+                    for (int e = 0; e < NE; ++e) {
+                        float t = vop_apply<EXACT>(ops, x[e], y[u][e]);
+                        t = sop_apply(ops, t, p.alpha, p.k);
+                        float w;
+                        if (ops.mop() == FMM_MOP_SEL2ND) {
+                            w = y[u][e];
+                        } else {
+                            if (ops.aop() == FMM_AOP_ASUM) {
+                                z[e] = fmac<EXACT>(z[e], a[u], t);
+                                continue;
+                            }
+                            w = fmul<EXACT>(a[u], t);
+                        }
+                        z[e] = aop_apply<EXACT>(ops, z[e], w);
+                    }
+                }
+            }
+        }
+    }
+
+    if (active) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i)
+            if (elem_ok[i]) store_vec<VEC>(out + (i * LPR + gl) * VEC, &z[i * VEC]);
+    }
+}
+
+#ifdef FMM_AUX_KERNELS
+// Fold chunk partials of split rows into Z in chunk order (deterministic).
+// split = {row, first slot, nchunks, 0}. Q chunk lanes per element each fold
+// a contiguous chunk range, then lane 0 folds the Q results in order.
+__global__ void __launch_bounds__(256)
+fmm_combine_kernel(const int4* __restrict__ split, const float* __restrict__ partial,
+                   float* __restrict__ Z, int d, int is_max) {
+    __shared__ float red[256];
+    const int4 s = split[blockIdx.x];
+    const int K = s.z;
+    const float* base = partial + static_cast<int64_t>(s.y) * d;
+    float* zr = Z + static_cast<int64_t>(s.x) * d;
+    const float ident = is_max ? -__int_as_float(0x7f800000) : 0.0f;
+    if (d >= 256) {
+        for (int j = threadIdx.x; j < d; j += 256) {
+            float acc = ident;
+            int k = 0;
+            for (; k + 4 <= K; k += 4) {
+                const float v0 = base[(int64_t)(k + 0) * d + j];
+                const float v1 = base[(int64_t)(k + 1) * d + j];
+                const float v2 = base[(int64_t)(k + 2) * d + j];
+                const float v3 = base[(int64_t)(k + 3) * d + j];
+                if (is_max) {
+                    acc = acc < v0 ? v0 : acc; acc = acc < v1 ? v1 : acc;
+                    acc = acc < v2 ? v2 : acc; acc = acc < v3 ? v3 : acc;
+                } else {
+                    acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, v0), v1), v2), v3);
+                }
+            }
+            for (; k < K; ++k) {
+                const float v = base[(int64_t)k * d + j];
+                acc = is_max ? (acc < v ? v : acc) : __fadd_rn(acc, v);
+            }
+            zr[j] = acc;
+        }
+        return;
+    }
+    const int Q = 256 / d;
+    const int q = threadIdx.x / d;
+    const int j = threadIdx.x % d;
+    if (q < Q) {
+        const int k0 = static_cast<int>((static_cast<int64_t>(K) * q) / Q);
+        const int k1 = static_cast<int>((static_cast<int64_t>(K) * (q + 1)) / Q);
+        float acc = ident;
+        int k = k0;
+        for (; k + 4 <= k1; k += 4) {
+            const float v0 = base[(int64_t)(k + 0) * d + j];
+            const float v1 = base[(int64_t)(k + 1) * d + j];
+            const float v2 = base[(int64_t)(k + 2) * d + j];
+            const float v3 = base[(int64_t)(k + 3) * d + j];
+            if (is_max) {
+                acc = acc < v0 ? v0 : acc; acc = acc < v1 ? v1 : acc;
+                acc = acc < v2 ? v2 : acc; acc = acc < v3 ? v3 : acc;
+            } else {
+                acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, v0), v1), v2), v3);
+            }
+        }
+        for (; k < k1; ++k) {
+            const float v = base[(int64_t)k * d + j];
+            acc = is_max ? (acc < v ? v : acc) : __fadd_rn(acc, v);
+        }
+        red[threadIdx.x] = acc;
+    }
+    __syncthreads();
+    if (q == 0) {
+        float acc = red[j];
+        for (int qq = 1; qq < Q; ++qq) {
+            const float v = red[qq * d + j];
+            acc = is_max ? (acc < v ? v : acc) : __fadd_rn(acc, v);
+        }
+        zr[j] = acc;
+    }
+}
+
+// Narrow int64 columns to int32 while validating 0 <= c < n; tracks max col.
+__global__ void fmm_narrow_cols_kernel(const int64_t* __restrict__ src, int32_t* __restrict__ dst,
+                                       int64_t count, int64_t n, int* __restrict__ bad,
+                                       int* __restrict__ max_col) {
+    int local_max = -1;
+    bool local_bad = false;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t c = src[i];
+        if (c < 0 || c >= n) {
+            local_bad = true;
+            dst[i] = 0;
+        } else {
+            dst[i] = static_cast<int32_t>(c);
+            local_max = max(local_max, static_cast<int>(c));
+        }
+    }
+    local_max = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(local_max + 1))) - 1;
+    if ((threadIdx.x & 31) == 0 && local_max >= 0) atomicMax(max_col, local_max);
+    if (local_bad) atomicExch(bad, 1);
+}
+
+#endif  // FMM_AUX_KERNELS
+
+// Launch descriptor shared by the dispatch translation units.
+struct LaunchCfg {
+    int pattern;   // FMM_PATTERN_*
+    int d;
+    bool exact;
+    bool aligned;  // X/Y/Z 16-byte aligned rows
+};
+
+// Defined in fmm_dispatch_*.cu; returns false if no instantiation fits.
+bool launch_rows(const KParams& p, const LaunchCfg& cfg, cudaStream_t stream);
+
+}  // namespace fmm

@@ -1,0 +1,98 @@
+// fmm_plan.cpp — see fmm_plan.h.
+#include "fmm_plan.h"
+
+#include <algorithm>
+#include <stdexcept>
+
+namespace fmm {
+
+std::vector<int64_t> part1d(int64_t m, const int64_t* row_ptr, int t) {
+    if (t < 1) throw std::invalid_argument("part1d: worker count must be >= 1");
+    std::vector<int64_t> b(static_cast<size_t>(t) + 1, 0);
+    b[0] = 0;
+    b[t] = m;
+    const int64_t base = m >= 0 ? row_ptr[0] : 0;
+    const int64_t nnz = row_ptr[m] - base;
+    if (nnz == 0) {
+        for (int i = 1; i < t; ++i) b[i] = m * i / t;
+        return b;
+    }
+    int64_t row = 0;
+    for (int i = 1; i < t; ++i) {
+        while (row < m && (row_ptr[row] - base) * static_cast<int64_t>(t) <
+                              static_cast<int64_t>(i) * nnz)
+            ++row;
+        b[i] = row;
+    }
+    return b;
+}
+
+std::string validate_row_ptr(int64_t m, const int64_t* row_ptr) {
+    if (m < 0) return "negative row count";
+    if (row_ptr[0] != 0) return "row_ptr[0] != 0";
+    for (int64_t i = 1; i <= m; ++i)
+        if (row_ptr[i] < row_ptr[i - 1])
+            return "row_ptr not monotone at index " + std::to_string(i);
+    return {};
+}
+
+namespace {
+// Degree bucket: 0 for empty rows, else 1 + 4*floor(log2 deg) + next two bits.
+inline int degree_bucket(int64_t deg) {
+    if (deg <= 0) return 0;
+    const int lg = 63 - __builtin_clzll(static_cast<unsigned long long>(deg));
+    const int frac = lg >= 2 ? static_cast<int>((deg >> (lg - 2)) & 3) : static_cast<int>((deg << (2 - lg)) & 3);
+    return 1 + 4 * lg + frac;
+}
+}  // namespace
+
+ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t row_end) {
+    ShardPlan P;
+    P.row_begin = row_begin;
+    P.row_end = row_end;
+    P.edge_begin = row_ptr[row_begin];
+    P.nnz = row_ptr[row_end] - row_ptr[row_begin];
+    const int64_t rows = row_end - row_begin;
+    if (rows > INT32_MAX) throw std::invalid_argument("shard has more than 2^31-1 rows");
+    P.local_row_ptr.resize(static_cast<size_t>(rows) + 1);
+    for (int64_t i = 0; i <= rows; ++i) P.local_row_ptr[i] = row_ptr[row_begin + i] - P.edge_begin;
+
+    // counting sort by (split?, bucket) descending, stable
+    constexpr int kBuckets = 1 + 4 * 64 + 4;
+    constexpr int kKeys = 2 * kBuckets;
+    std::vector<int64_t> count(kKeys + 1, 0);
+    auto key_of = [&](int64_t r) {
+        const int64_t deg = P.local_row_ptr[r + 1] - P.local_row_ptr[r];
+        const int split = deg > kChunkEdges ? 1 : 0;
+        // descending: larger key first
+        return kKeys - 1 - (split * kBuckets + degree_bucket(deg));
+    };
+    for (int64_t r = 0; r < rows; ++r) {
+        const int64_t deg = P.local_row_ptr[r + 1] - P.local_row_ptr[r];
+        if (deg > 0) ++P.nonempty_rows;
+        P.max_degree = std::max(P.max_degree, deg);
+        if (deg > kChunkEdges) ++P.n_split_rows;
+        ++count[key_of(r) + 1];
+    }
+    for (int k = 0; k < kKeys; ++k) count[k + 1] += count[k];
+    P.order.resize(static_cast<size_t>(rows));
+    for (int64_t r = 0; r < rows; ++r) P.order[count[key_of(r)]++] = static_cast<int32_t>(r);
+
+    // chunk items for the split prefix, slots assigned row by row
+    int64_t slot = 0;
+    P.split_rows.reserve(static_cast<size_t>(P.n_split_rows));
+    for (int64_t i = 0; i < P.n_split_rows; ++i) {
+        const int32_t r = P.order[i];
+        const int64_t deg = P.local_row_ptr[r + 1] - P.local_row_ptr[r];
+        const int64_t nch = (deg + kChunkEdges - 1) / kChunkEdges;
+        if (slot + nch > INT32_MAX) throw std::invalid_argument("too many chunk slots");
+        P.split_rows.push_back({r, static_cast<int32_t>(slot), static_cast<int32_t>(nch), 0});
+        for (int64_t k = 0; k < nch; ++k)
+            P.chunks.push_back({r, static_cast<int32_t>(k), static_cast<int32_t>(slot + k), 0});
+        slot += nch;
+    }
+    P.n_slots = slot;
+    return P;
+}
+
+}  // namespace fmm

@@ -1,0 +1,52 @@
+// fmm_plan.h — host-side planning for the device FusedMM path.
+//
+// Everything here runs once per graph upload (excluded from kernel timing,
+// like the paper's preprocessing): the part1d row partition,
+// CSR validation, and the per-shard work lists the row kernels consume.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace fmm {
+
+// Edges per chunk when a heavy row is split on the reassociating scheme.
+// Chunk boundaries sit at fixed row-relative offsets, so results do not
+// depend on the shard count.
+constexpr int kChunkEdges = 256;
+
+struct Int4 {
+    int32_t x, y, z, w;
+};
+
+// part1d (kernel.hpp:24-49): boundary i is the smallest row r with
+// row_ptr[r]*t >= i*nnz; rows split evenly when nnz == 0. row_ptr may be a
+// rebased sub-range (row_ptr[0] subtracted by the caller or not: the rule is
+// applied to row_ptr[r] - row_ptr[0]).
+std::vector<int64_t> part1d(int64_t m, const int64_t* row_ptr, int t);
+
+// Validates row_ptr over [row_begin, row_end]: monotone, row_ptr[0] == 0.
+// Returns an empty string when valid, else the first violation.
+std::string validate_row_ptr(int64_t m, const int64_t* row_ptr);
+
+// Work lists for one shard (rows [row_begin, row_end), local row ids).
+struct ShardPlan {
+    int64_t row_begin = 0, row_end = 0;   // absolute
+    int64_t edge_begin = 0, nnz = 0;      // absolute edge offset, count
+    std::vector<int64_t> local_row_ptr;   // rebased, rows+1
+    // Rows ordered heavy-first: rows with degree > kChunkEdges first, then by
+    // descending log2-quarter degree bucket, stable (natural order) inside a
+    // bucket so light rows keep their memory locality.
+    std::vector<int32_t> order;
+    int64_t n_split_rows = 0;             // prefix of `order` cut into chunks
+    std::vector<Int4> chunks;             // {row, k, slot, 0}
+    std::vector<Int4> split_rows;         // {row, first slot, nchunks, 0}
+    int64_t n_slots = 0;
+    int64_t nonempty_rows = 0;
+    int64_t max_degree = 0;
+};
+
+ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t row_end);
+
+}  // namespace fmm

@@ -1,0 +1,628 @@
+"""Python mirror of the reference FusedMM interface, running on the B200 path.
+
+Names, argument meaning and error behaviour follow the reference headers:
+
+    index_t, DenseMatrix, CsrMatrix, csr_from_coo, validate, stats
+                                        proj/include/fusedmm/matrix.hpp:15-180
+    Vop/Rop/Sop/Mop/Aop, KnownPattern, OpSpec, pattern_of
+                                        proj/include/fusedmm/ops.hpp:14-51,189-203
+    part1d, PartitionPlan, KernelStats, KernelOptions, fused_mm,
+    fused_mm_specialized                proj/include/fusedmm/kernel.hpp:16-378
+    App, AppParams, make_spec, fr_layout_sub_spec, embedding_step,
+    fr_layout_step, gcn_forward         proj/include/fusedmm/apps.hpp:12-88
+
+std::invalid_argument -> InvalidArgument (a ValueError), std::logic_error ->
+LogicError. `t`, the reference's worker count, is the number of GPU shards.
+Every fused call goes through libfusedmm_cuda's C ABI; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import fmm_graph_info, fmm_opspec, fmm_stats
+
+index_t = np.int64
+
+
+# ----------------------------------------------------------------- errors
+class FusedMMError(RuntimeError):
+    pass
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class LogicError(FusedMMError):
+    """std::logic_error in the reference."""
+
+
+class Unsupported(NotImplementedError):
+    """A USER slot or shape with no device kernel (no CPU fallback)."""
+
+
+class CudaError(FusedMMError):
+    pass
+
+
+class DeviceOutOfMemory(MemoryError):
+    pass
+
+
+def _raise(status: int, ctx=None, what: str = "") -> None:
+    if status == _lib.FMM_OK:
+        return
+    msg = what
+    if ctx is not None:
+        e = _lib.lib().fmm_last_error(ctx)
+        if e:
+            msg = e.decode()
+    cls = {
+        _lib.FMM_E_INVAL: InvalidArgument,
+        _lib.FMM_E_UNSUPPORTED: Unsupported,
+        _lib.FMM_E_CUDA: CudaError,
+        _lib.FMM_E_NCCL: CudaError,
+        _lib.FMM_E_OOM: DeviceOutOfMemory,
+        _lib.FMM_E_LOGIC: LogicError,
+    }.get(status, FusedMMError)
+    raise cls(msg or _lib.lib().fmm_status_string(status).decode())
+
+
+# ---------------------------------------------------------------- op enums
+class Vop(enum.IntEnum):
+    ADD = 0
+    MUL = 1
+    SEL2ND = 2
+    SUB = 3
+    USER = 4
+
+
+class Rop(enum.IntEnum):
+    NOOP = 0
+    RSUM = 1
+    RMUL = 2
+    NORM = 3
+    USER = 4
+    SQNORM = 16  # device extension: sum of squares, no sqrt
+
+
+class Sop(enum.IntEnum):
+    NOOP = 0
+    SIGMOID = 1
+    SCAL = 2
+    USER = 3
+    TDIST = 16  # device extension: 1/(1+s)
+    SQK = 17    # device extension: s/k
+
+
+class Mop(enum.IntEnum):
+    MUL = 0
+    SEL2ND = 1
+    USER = 2
+    MUL_VOP = 16  # device extension: w = a_uv*(h*t), t the VOP output
+
+
+class Aop(enum.IntEnum):
+    ASUM = 0
+    AMAX = 1
+    USER = 2
+
+
+class KnownPattern(enum.IntEnum):
+    SIGMOID_EMBED = 0
+    SPMM_GCN = 1
+    FR_LAYOUT = 2
+    GENERIC = 3
+    TDIST = 16
+    FR_ATTRACT = 17
+
+
+@dataclass
+class OpSpec:
+    """OpSpec<T> (ops.hpp:22-51). USER hooks are accepted for interface parity
+    but have no device kernel: fused_mm raises Unsupported for them."""
+    vop: Vop = Vop.MUL
+    rop: Rop = Rop.RSUM
+    sop: Sop = Sop.NOOP
+    mop: Mop = Mop.MUL
+    aop: Aop = Aop.ASUM
+    alpha: float = 1.0
+    k: float = 1.0
+    user_vop: Optional[Callable] = None
+    user_rop: Optional[Callable] = None
+    user_sop: Optional[Callable] = None
+    user_mop: Optional[Callable] = None
+    user_aop: Optional[Callable] = None
+
+    def scalar_message(self) -> bool:  # ops.hpp:45
+        return self.rop != Rop.NOOP
+
+    def has_user_slot(self) -> bool:  # ops.hpp:47-50
+        return (self.vop == Vop.USER or self.rop == Rop.USER or self.sop == Sop.USER
+                or self.mop == Mop.USER or self.aop == Aop.USER)
+
+    def to_c(self) -> fmm_opspec:
+        return fmm_opspec(int(self.vop), int(self.rop), int(self.sop), int(self.mop),
+                          int(self.aop), float(self.alpha), float(self.k))
+
+
+def pattern_of(spec: OpSpec) -> KnownPattern:
+    """ops.hpp:189-203 (+ the two device-only patterns), via the C ABI."""
+    out = C.c_int32()
+    _raise(_lib.lib().fmm_pattern_of(C.byref(spec.to_c()), C.byref(out)))
+    return KnownPattern(out.value)
+
+
+# -------------------------------------------------------------- containers
+class DenseMatrix:
+    """Row-major nrows x dim float32 matrix (matrix.hpp:18-44)."""
+
+    def __init__(self, rows: int, d: int, values=None, fill: float = 0.0):
+        self.nrows = int(rows)
+        self.dim = int(d)
+        if values is None:
+            self.data = np.full(self.nrows * self.dim, fill, dtype=np.float32)
+        else:
+            arr = np.ascontiguousarray(np.asarray(values, dtype=np.float32).reshape(-1))
+            if arr.size != self.nrows * self.dim:
+                raise InvalidArgument("DenseMatrix: data length != nrows*dim")
+            if not np.all(np.isfinite(arr)):
+                raise InvalidArgument("DenseMatrix: non-finite value")
+            self.data = arr
+
+    @classmethod
+    def wrap(cls, arr: np.ndarray) -> "DenseMatrix":
+        """Adopt a contiguous float32 (rows, d) array without the finite check."""
+        a = np.ascontiguousarray(arr, dtype=np.float32)
+        M = cls.__new__(cls)
+        M.nrows, M.dim = int(a.shape[0]), int(a.shape[1])
+        M.data = a.reshape(-1)
+        return M
+
+    @property
+    def array(self) -> np.ndarray:
+        return self.data.reshape(self.nrows, self.dim)
+
+    def row(self, u: int) -> np.ndarray:
+        return self.data[u * self.dim:(u + 1) * self.dim]
+
+    def at(self, u: int, j: int) -> float:
+        return float(self.data[u * self.dim + j])
+
+
+@dataclass
+class GraphStats:
+    nrows: int = 0
+    ncols: int = 0
+    nnz: int = 0
+    avg_degree: float = 0.0
+    max_degree: int = 0
+
+
+class CsrMatrix:
+    """CSR adjacency with int64 indices (matrix.hpp:48-68). Per-row storage
+    order is the accumulation order of every kernel."""
+
+    def __init__(self, nrows: int = 0, ncols: int = 0, row_ptr=None, col_idx=None, values=None):
+        self.nrows = int(nrows)
+        self.ncols = int(ncols)
+        self.row_ptr = (np.zeros(self.nrows + 1, dtype=np.int64) if row_ptr is None
+                        else np.ascontiguousarray(row_ptr, dtype=np.int64))
+        self.col_idx = (np.zeros(0, dtype=np.int64) if col_idx is None
+                        else np.ascontiguousarray(col_idx, dtype=np.int64))
+        if values is None:
+            self.values = np.ones(self.col_idx.size, dtype=np.float32)
+            self.unit_values = True
+        else:
+            self.values = np.ascontiguousarray(values, dtype=np.float32)
+            self.unit_values = False
+        self._device = {}
+
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1]) if self.row_ptr.size else 0
+
+    def row_nnz(self, u: int) -> int:
+        return int(self.row_ptr[u + 1] - self.row_ptr[u])
+
+    def row_cols(self, u: int) -> np.ndarray:
+        return self.col_idx[self.row_ptr[u]:self.row_ptr[u + 1]]
+
+    def row_vals(self, u: int) -> np.ndarray:
+        return self.values[self.row_ptr[u]:self.row_ptr[u + 1]]
+
+    def invalidate(self) -> None:
+        """Drop cached device copies after mutating the arrays in place."""
+        for g in self._device.values():
+            g.free()
+        self._device.clear()
+
+
+def csr_from_coo(entries: Sequence[tuple], m: int, n: int) -> CsrMatrix:
+    """matrix.hpp:87-140: duplicates summed, per-row storage order is the
+    first-occurrence order of the deduplicated entries."""
+    for (r, c, _v) in entries:
+        if r < 0 or r >= m or c < 0 or c >= n:
+            raise InvalidArgument(f"csr_from_coo: entry ({r},{c}) out of bounds for {m}x{n}")
+    rows: list[list] = [[] for _ in range(m)]
+    for (r, c, v) in entries:
+        rows[r].append((c, v))
+    row_ptr = np.zeros(m + 1, dtype=np.int64)
+    cols: list[int] = []
+    vals: list[float] = []
+    for r in range(m):
+        pos: dict[int, int] = {}
+        for (c, v) in rows[r]:
+            if c in pos:
+                vals[pos[c]] = np.float32(vals[pos[c]]) + np.float32(v)
+            else:
+                pos[c] = len(cols)
+                cols.append(c)
+                vals.append(np.float32(v))
+        row_ptr[r + 1] = len(cols)
+    return CsrMatrix(m, n, row_ptr, np.array(cols, dtype=np.int64),
+                     np.array(vals, dtype=np.float32))
+
+
+def validate(A: CsrMatrix) -> Optional[str]:
+    """matrix.hpp:143-166: first CSR invariant violation, or None."""
+    if A.row_ptr.size != A.nrows + 1:
+        return "row_ptr length is not nrows+1"
+    if A.row_ptr[0] != 0:
+        return "row_ptr[0] != 0"
+    dif = np.diff(A.row_ptr)
+    if np.any(dif < 0):
+        return f"row_ptr not monotone at index {int(np.argmax(dif < 0)) + 1}"
+    if A.col_idx.size != A.row_ptr[-1]:
+        return "col_idx length != row_ptr[nrows]"
+    if A.values.size != A.col_idx.size:
+        return "values length != col_idx length"
+    if A.col_idx.size and (A.col_idx.min() < 0 or A.col_idx.max() >= A.ncols):
+        return "column index out of range"
+    rows = np.repeat(np.arange(A.nrows, dtype=np.int64), dif)
+    key = rows * max(A.ncols, 1) + A.col_idx
+    if np.unique(key).size != key.size:
+        bad = rows[np.argsort(key)][np.r_[np.diff(np.sort(key)) == 0, False]][0]
+        return f"duplicate column in row {int(bad)}"
+    return None
+
+
+def stats(A: CsrMatrix) -> GraphStats:
+    """matrix.hpp:168-180."""
+    nnz = A.nnz()
+    deg = np.diff(A.row_ptr)
+    return GraphStats(A.nrows, A.ncols, nnz, nnz / A.nrows if A.nrows else 0.0,
+                      int(deg.max()) if deg.size else 0)
+
+
+# --------------------------------------------------------------- partition
+@dataclass
+class PartitionPlan:
+    boundaries: list
+    workers: int = 0
+
+
+def part1d(A: CsrMatrix, t: int) -> PartitionPlan:
+    """kernel.hpp:24-49 through the library's host implementation."""
+    if t < 1:
+        raise InvalidArgument("part1d: worker count must be >= 1")
+    b = np.zeros(t + 1, dtype=np.int64)
+    _raise(_lib.lib().fmm_part1d(A.nrows, _i64(A.row_ptr), t, _i64(b)))
+    return PartitionPlan([int(x) for x in b], t)
+
+
+@dataclass
+class KernelStats:
+    """kernel.hpp:51-55 (+ device evidence)."""
+    aux_bytes: int = 0
+    threads: int = 0
+    pattern: KnownPattern = KnownPattern.GENERIC
+    exact: bool = False
+    launches: int = 0
+    kernel_ms: float = 0.0
+    total_ms: float = 0.0
+
+    def fill(self, s: fmm_stats) -> None:
+        self.aux_bytes = int(s.aux_bytes)
+        self.threads = int(s.threads)
+        self.pattern = KnownPattern(s.pattern)
+        self.exact = bool(s.exact)
+        self.launches = int(s.launches)
+        self.kernel_ms = float(s.kernel_ms)
+        self.total_ms = float(s.total_ms)
+
+
+@dataclass
+class KernelOptions:
+    """kernel.hpp:286-288. lane_width is the CPU lane-blocking width; on the
+    device it is validated for interface parity (the lane mapping is fixed
+    by d). exact: None = per-pattern default, True/False = force."""
+    lane_width: int = 8
+    exact: Optional[bool] = None
+
+
+# ------------------------------------------------------------ ctypes utils
+def _i64(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int64))
+
+
+def _f32(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def _vp(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data)
+
+
+# ----------------------------------------------------------- device objects
+class Context:
+    """An fmm_ctx: one shard (CUDA stream) per entry of `devices`."""
+
+    def __init__(self, devices: Sequence[int]):
+        L = _lib.lib()
+        self.devices = list(devices)
+        arr = (C.c_int * len(self.devices))(*self.devices)
+        h = C.c_void_p()
+        st = L.fmm_create(len(self.devices), arr, C.byref(h))
+        if st != _lib.FMM_OK:
+            _raise(st, None, "fmm_create failed (no CUDA device?)")
+        self.h = h
+
+    def set_stream(self, shard: int, stream_handle: int) -> None:
+        _raise(_lib.lib().fmm_set_stream(self.h, shard, C.c_void_p(stream_handle)), self.h)
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            _lib.lib().fmm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_contexts: dict = {}
+
+
+def device_count() -> int:
+    return int(_lib.lib().fmm_device_count())
+
+
+def default_context(t: int) -> Context:
+    """Context with t shards over the visible GPUs (round-robin)."""
+    if t not in _contexts:
+        n = device_count()
+        if n < 1:
+            raise CudaError("no CUDA device visible (libfusedmm_cuda has no CPU fallback)")
+        _contexts[t] = Context([i % n for i in range(t)])
+    return _contexts[t]
+
+
+class DeviceGraph:
+    """A CSR uploaded once (fmm_graph), optionally only rows [row_begin, row_end)."""
+
+    def __init__(self, ctx: Context, A: CsrMatrix, row_begin: int = 0, row_end: Optional[int] = None):
+        self.ctx = ctx
+        self.A = A
+        rb = 0 if row_begin is None else int(row_begin)
+        re = A.nrows if row_end is None else int(row_end)
+        h = C.c_void_p()
+        vals = None if A.unit_values else _f32(A.values)
+        st = _lib.lib().fmm_graph_upload(ctx.h, A.nrows, A.ncols, _i64(A.row_ptr), _i64(A.col_idx),
+                                         vals, rb, re, C.byref(h))
+        _raise(st, ctx.h)
+        self.h = h
+        self.row_begin, self.row_end = rb, re
+
+    def info(self) -> fmm_graph_info:
+        I = fmm_graph_info()
+        _raise(_lib.lib().fmm_graph_get_info(self.h, C.byref(I)))
+        return I
+
+    def shard_bounds(self) -> list:
+        I = self.info()
+        b = np.zeros(I.shards + 1, dtype=np.int64)
+        _raise(_lib.lib().fmm_graph_shard_bounds(self.h, _i64(b)))
+        return [int(x) for x in b]
+
+    def run_host(self, X: np.ndarray, Y: np.ndarray, Z: np.ndarray, d: int, spec: OpSpec,
+                 flags: int = 0) -> fmm_stats:
+        s = fmm_stats()
+        st = _lib.lib().fmm_run(self.ctx.h, self.h, C.byref(spec.to_c()), d, _vp(X),
+                                Y.shape[0] if Y.ndim == 2 else Y.size // max(d, 1), _vp(Y), _vp(Z),
+                                flags, C.byref(s))
+        _raise(st, self.ctx.h)
+        return s
+
+    def run_device(self, x_ptr: int, ny: int, y_ptr: int, z_ptr: int, d: int, spec: OpSpec,
+                   flags: int = _lib.FMM_DEVICE_PTRS | _lib.FMM_ASYNC,
+                   stats: Optional[fmm_stats] = None) -> None:
+        st = _lib.lib().fmm_run(self.ctx.h, self.h, C.byref(spec.to_c()), d, C.c_void_p(x_ptr), ny,
+                                C.c_void_p(y_ptr), C.c_void_p(z_ptr), flags,
+                                C.byref(stats) if stats is not None else None)
+        _raise(st, self.ctx.h)
+
+    def iterate_host(self, X: np.ndarray, d: int, spec: OpSpec, iters: int, flags: int = 0) -> fmm_stats:
+        s = fmm_stats()
+        st = _lib.lib().fmm_iterate(self.ctx.h, self.h, C.byref(spec.to_c()), d, _vp(X), iters, flags,
+                                    C.byref(s))
+        _raise(st, self.ctx.h)
+        return s
+
+    def free(self) -> None:
+        if getattr(self, "h", None):
+            _lib.lib().fmm_graph_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _device_graph(A: CsrMatrix, t: int) -> DeviceGraph:
+    key = (t, A.row_ptr.ctypes.data, A.col_idx.ctypes.data, A.values.ctypes.data, A.nnz())
+    g = A._device.get(t)
+    if g is None or g._key != key:
+        if g is not None:
+            g.free()
+        g = DeviceGraph(default_context(t), A)
+        g._key = key
+        A._device[t] = g
+    return g
+
+
+# ------------------------------------------------------------- entry points
+def _check_dims(A: CsrMatrix, X: DenseMatrix, Y: DenseMatrix) -> None:
+    """kernel.hpp:269-282, same messages."""
+    if X.nrows != A.nrows:
+        raise InvalidArgument("fused_mm: X.nrows != A.nrows")
+    if X.dim != Y.dim:
+        raise InvalidArgument("fused_mm: X.dim != Y.dim")
+    if Y.nrows < A.ncols and A.nnz() > 0 and Y.nrows < int(A.col_idx.max()) + 1:
+        raise InvalidArgument("fused_mm: Y has too few rows")
+
+
+def _flags(opts: Optional[KernelOptions]) -> int:
+    if opts is None:
+        return 0
+    if opts.lane_width not in (4, 8, 16):
+        raise InvalidArgument("KernelOptions.lane_width must be 4, 8 or 16")
+    if opts.exact is True:
+        return _lib.FMM_EXACT
+    if opts.exact is False:
+        return _lib.FMM_FAST
+    return 0
+
+
+def fused_mm(A: CsrMatrix, X: DenseMatrix, Y: DenseMatrix, spec: OpSpec, t: int = 1,
+             stats: Optional[KernelStats] = None, opts: Optional[KernelOptions] = None) -> DenseMatrix:
+    """kernel.hpp:297-353 on the B200: Z[u,:] = update_u(a_u, x_u, Y, spec)
+    for every row, one pass, no per-edge message buffer. t = GPU shards."""
+    _check_dims(A, X, Y)
+    if t < 1:
+        raise InvalidArgument("fused_mm: t must be >= 1")
+    if spec.has_user_slot():
+        raise Unsupported("fused_mm: USER slot has no device kernel (no CPU fallback)")
+    flags = _flags(opts)
+    Z = DenseMatrix(A.nrows, X.dim)
+    if A.nrows == 0:
+        if stats is not None:
+            stats.threads, stats.pattern = t, pattern_of(spec)
+        return Z
+    g = _device_graph(A, t)
+    Xd = X.data if X.data.size else np.zeros(1, np.float32)
+    Yd = Y.data if Y.data.size else np.zeros(1, np.float32)
+    s = fmm_stats()
+    st = _lib.lib().fmm_run(g.ctx.h, g.h, C.byref(spec.to_c()), X.dim, _vp(Xd), Y.nrows,
+                            _vp(Xd) if Y is X else _vp(Yd), _vp(Z.data), flags, C.byref(s))
+    _raise(st, g.ctx.h)
+    if stats is not None:
+        stats.fill(s)
+    return Z
+
+
+def fused_mm_specialized(pattern: KnownPattern, A: CsrMatrix, X: DenseMatrix, Y: DenseMatrix,
+                         alpha: float, t: int = 1, opts: Optional[KernelOptions] = None) -> DenseMatrix:
+    """kernel.hpp:356-378."""
+    if pattern == KnownPattern.SIGMOID_EMBED:
+        spec = OpSpec(Vop.MUL, Rop.RSUM, Sop.SIGMOID, Mop.MUL, Aop.ASUM)
+    elif pattern == KnownPattern.SPMM_GCN:
+        spec = OpSpec(Vop.SEL2ND, Rop.NOOP, Sop.NOOP, Mop.MUL, Aop.ASUM)
+    elif pattern == KnownPattern.FR_LAYOUT:
+        spec = OpSpec(Vop.ADD, Rop.NORM, Sop.SCAL, Mop.MUL, Aop.ASUM, alpha=alpha)
+    elif pattern == KnownPattern.TDIST:
+        spec = tdist_spec()
+    elif pattern == KnownPattern.FR_ATTRACT:
+        spec = fr_attract_spec(alpha if alpha else 1.0)
+    else:
+        raise InvalidArgument("fused_mm_specialized: pattern has no fast path")
+    return fused_mm(A, X, X if Y is X else Y, spec, t, None, opts)
+
+
+def iterate(A: CsrMatrix, X: DenseMatrix, spec: OpSpec, iters: int, t: int = 1,
+            stats: Optional[KernelStats] = None, opts: Optional[KernelOptions] = None) -> DenseMatrix:
+    """iters fused calls with X <- Z (Y = X), resident on the device; with
+    t > 1 shards the Z slices are exchanged between shards each iteration."""
+    if A.nrows != A.ncols or X.nrows != A.nrows:
+        raise InvalidArgument("iterate: needs a square A and X.nrows == A.nrows")
+    if spec.has_user_slot():
+        raise Unsupported("iterate: USER slot has no device kernel")
+    out = DenseMatrix.wrap(X.array.copy())
+    if A.nrows == 0:
+        return out
+    g = _device_graph(A, t)
+    s = g.iterate_host(out.data, X.dim, spec, iters, _flags(opts))
+    if stats is not None:
+        stats.fill(s)
+    return out
+
+
+# ------------------------------------------------------------------ apps
+class App(enum.IntEnum):
+    FR_LAYOUT = 0
+    NODE_EMBED_SIGMOID = 1
+    GCN_FORWARD = 2
+    GNN_MLP = 3
+
+
+@dataclass
+class AppParams:
+    alpha: float = 1.0
+    mlp_vop: Optional[Callable] = None
+
+
+def make_spec(app: App, params: Optional[AppParams] = None) -> OpSpec:
+    """apps.hpp:22-45."""
+    params = params or AppParams()
+    if app == App.FR_LAYOUT:
+        return OpSpec(Vop.ADD, Rop.NORM, Sop.SCAL, Mop.MUL, Aop.ASUM, alpha=params.alpha)
+    if app == App.NODE_EMBED_SIGMOID:
+        return OpSpec(Vop.MUL, Rop.RSUM, Sop.SIGMOID, Mop.MUL, Aop.ASUM)
+    if app == App.GCN_FORWARD:
+        return OpSpec(Vop.SEL2ND, Rop.NOOP, Sop.NOOP, Mop.MUL, Aop.ASUM)
+    if app == App.GNN_MLP:
+        if params.mlp_vop is None:
+            raise InvalidArgument("make_spec: GNN_MLP needs a user-provided MLP function")
+        return OpSpec(Vop.USER, Rop.NOOP, Sop.SIGMOID, Mop.MUL, Aop.AMAX, user_vop=params.mlp_vop)
+    raise InvalidArgument("make_spec: unknown app")
+
+
+def fr_layout_sub_spec(alpha: float) -> OpSpec:
+    """apps.hpp:49-54."""
+    return OpSpec(Vop.SUB, Rop.NORM, Sop.SCAL, Mop.MUL, Aop.ASUM, alpha=alpha)
+
+
+def tdist_spec() -> OpSpec:
+    """Config 3 t-distribution layout: t = x_u - x_v, s = |t|^2,
+    h = 1/(1+s), w = a_uv*(h*t), summed (the reference's USER-VOP lambda)."""
+    return OpSpec(Vop.SUB, Rop.SQNORM, Sop.TDIST, Mop.MUL_VOP, Aop.ASUM)
+
+
+def fr_attract_spec(k: float = 1.0) -> OpSpec:
+    """Config 4 FR-attractive: h = |x_u - x_v|^2 / k scales the difference."""
+    return OpSpec(Vop.SUB, Rop.SQNORM, Sop.SQK, Mop.MUL_VOP, Aop.ASUM, k=k)
+
+
+def embedding_step(A: CsrMatrix, X: DenseMatrix, Y: DenseMatrix, t: int = 1) -> DenseMatrix:
+    """apps.hpp:67-71."""
+    return fused_mm(A, X, Y, make_spec(App.NODE_EMBED_SIGMOID), t)
+
+
+def fr_layout_step(A: CsrMatrix, X: DenseMatrix, Y: DenseMatrix, alpha: float, t: int = 1) -> DenseMatrix:
+    """apps.hpp:74-80."""
+    return fused_mm(A, X, Y, make_spec(App.FR_LAYOUT, AppParams(alpha=alpha)), t)
+
+
+def gcn_forward(A: CsrMatrix, Y: DenseMatrix, t: int = 1) -> DenseMatrix:
+    """apps.hpp:83-88 (X is a zero matrix; SEL2ND never reads it)."""
+    X = DenseMatrix(A.nrows, Y.dim)
+    return fused_mm(A, X, Y, make_spec(App.GCN_FORWARD), t)
