@@ -1,0 +1,245 @@
+// fusedmm_cuda.hpp — header-only C++ wrapper over libfusedmm_cuda's C ABI
+// with the reference driver's signature and exception behaviour:
+//
+//   reference:  fusedmm::fused_mm(A, X, Y, spec, t, stats, opts)
+//               (/root/reference/proj/include/fusedmm/kernel.hpp:297-353)
+//   here:       fusedmm::cuda::fused_mm(A, X, Y, spec, t, stats, opts)
+//
+// The wrapper is generic over the container types: it works with the
+// reference's own fusedmm::CsrMatrix<float> / DenseMatrix<float> /
+// OpSpec<float> / KernelStats / KernelOptions (so existing host code switches
+// by changing the namespace), and with the minimal mirrors in
+// fusedmm::cuda::types for code that does not include the reference.
+//
+// Errors: dimension mismatch and t < 1 throw std::invalid_argument exactly
+// where kernel.hpp:269-282,303 does; a USER slot (a std::function the device
+// cannot run) throws fusedmm::cuda::unsupported — there is no CPU fallback.
+// t is the number of GPU shards (devices 0..n-1 round-robin), the analogue of
+// the reference's worker threads; the result is bitwise independent of t.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "fusedmm_cuda.h"
+
+namespace fusedmm {
+namespace cuda {
+
+struct unsupported : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct device_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline void throw_status(fmm_status st, const fmm_ctx* ctx = nullptr) {
+    if (st == FMM_OK) return;
+    std::string msg = ctx ? fmm_last_error(ctx) : "";
+    if (msg.empty()) msg = fmm_status_string(st);
+    switch (st) {
+        case FMM_E_INVAL: throw std::invalid_argument(msg);
+        case FMM_E_LOGIC: throw std::logic_error(msg);
+        case FMM_E_UNSUPPORTED: throw unsupported(msg);
+        case FMM_E_OOM: throw std::bad_alloc();
+        default: throw device_error(msg);
+    }
+}
+
+// Minimal containers with the reference field names (matrix.hpp:18-68,
+// ops.hpp:22-51, kernel.hpp:51-55,286-288) for users without the reference.
+namespace types {
+enum class Vop { ADD, MUL, SEL2ND, SUB, USER };
+enum class Rop { NOOP, RSUM, RMUL, NORM, USER };
+enum class Sop { NOOP, SIGMOID, SCAL, USER };
+enum class Mop { MUL, SEL2ND, USER };
+enum class Aop { ASUM, AMAX, USER };
+enum class KnownPattern { SIGMOID_EMBED, SPMM_GCN, FR_LAYOUT, GENERIC };
+
+struct DenseMatrix {
+    int64_t nrows = 0, dim = 0;
+    std::vector<float> data;
+    DenseMatrix() = default;
+    DenseMatrix(int64_t rows, int64_t d, float fill = 0.f)
+        : nrows(rows), dim(d), data(static_cast<size_t>(rows * d), fill) {}
+};
+struct CsrMatrix {
+    int64_t nrows = 0, ncols = 0;
+    std::vector<int64_t> row_ptr{0}, col_idx;
+    std::vector<float> values;
+    int64_t nnz() const { return row_ptr.empty() ? 0 : row_ptr.back(); }
+};
+struct OpSpec {
+    Vop vop = Vop::MUL;
+    Rop rop = Rop::RSUM;
+    Sop sop = Sop::NOOP;
+    Mop mop = Mop::MUL;
+    Aop aop = Aop::ASUM;
+    float alpha = 1.f;
+};
+struct KernelStats {
+    std::size_t aux_bytes = 0;
+    int threads = 0;
+    KnownPattern pattern = KnownPattern::GENERIC;
+};
+struct KernelOptions {
+    int lane_width = 8;
+};
+}  // namespace types
+
+// Device-only op descriptor for the patterns the reference can only express
+// through a USER VOP lambda (configs 3 and 4).
+inline fmm_opspec tdist_ops() {
+    return fmm_opspec{FMM_VOP_SUB, FMM_ROP_SQNORM, FMM_SOP_TDIST, FMM_MOP_MUL_VOP, FMM_AOP_ASUM, 1.f, 1.f};
+}
+inline fmm_opspec fr_attract_ops(float k) {
+    return fmm_opspec{FMM_VOP_SUB, FMM_ROP_SQNORM, FMM_SOP_SQK, FMM_MOP_MUL_VOP, FMM_AOP_ASUM, 1.f, k};
+}
+
+// One context per shard count, one uploaded graph cached per context.
+class Context {
+public:
+    explicit Context(int t) {
+        const int ndev = fmm_device_count();
+        if (ndev < 1) throw device_error("fusedmm::cuda: no CUDA device (no CPU fallback)");
+        std::vector<int> devs(static_cast<size_t>(t));
+        for (int i = 0; i < t; ++i) devs[i] = i % ndev;
+        throw_status(fmm_create(t, devs.data(), &ctx_));
+    }
+    ~Context() {
+        if (graph_) fmm_graph_free(graph_);
+        if (ctx_) fmm_destroy(ctx_);
+    }
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+
+    static Context& for_shards(int t) {
+        static std::mutex mu;
+        static std::vector<std::unique_ptr<Context>> pool;
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto& c : pool)
+            if (c->t_ == t) return *c;
+        pool.emplace_back(new Context(t));
+        pool.back()->t_ = t;
+        return *pool.back();
+    }
+
+    // Upload A unless it is the graph uploaded last (same arrays, same size).
+    template <class Csr>
+    fmm_graph* graph_for(const Csr& A) {
+        const void* key[4] = {A.row_ptr.data(), A.col_idx.data(), A.values.data(),
+                              reinterpret_cast<const void*>(static_cast<intptr_t>(A.nnz()))};
+        if (graph_ && std::memcmp(key, key_, sizeof(key)) == 0 && m_ == A.nrows) return graph_;
+        if (graph_) fmm_graph_free(graph_);
+        graph_ = nullptr;
+        throw_status(fmm_graph_upload(ctx_, A.nrows, A.ncols, A.row_ptr.data(),
+                                      A.col_idx.empty() ? nullptr : A.col_idx.data(),
+                                      A.values.empty() ? nullptr : A.values.data(), 0, A.nrows,
+                                      &graph_),
+                     ctx_);
+        std::memcpy(key_, key, sizeof(key));
+        m_ = A.nrows;
+        return graph_;
+    }
+    fmm_ctx* get() const { return ctx_; }
+
+private:
+    fmm_ctx* ctx_ = nullptr;
+    fmm_graph* graph_ = nullptr;
+    const void* key_[4] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t m_ = -1;
+    int t_ = 0;
+};
+
+namespace detail {
+
+// kernel.hpp:269-282, same conditions and messages
+template <class Csr, class Dense>
+void check_dims(const Csr& A, const Dense& X, const Dense& Y) {
+    if (X.nrows != A.nrows) throw std::invalid_argument("fused_mm: X.nrows != A.nrows");
+    if (X.dim != Y.dim) throw std::invalid_argument("fused_mm: X.dim != Y.dim");
+    if (Y.nrows < A.ncols) {
+        int64_t max_col = -1;
+        for (auto c : A.col_idx) max_col = std::max<int64_t>(max_col, c);
+        if (Y.nrows < max_col + 1) throw std::invalid_argument("fused_mm: Y has too few rows");
+    }
+}
+
+template <class Spec>
+fmm_opspec to_c(const Spec& s) {
+    return fmm_opspec{static_cast<int32_t>(s.vop), static_cast<int32_t>(s.rop),
+                      static_cast<int32_t>(s.sop), static_cast<int32_t>(s.mop),
+                      static_cast<int32_t>(s.aop), static_cast<float>(s.alpha), 1.f};
+}
+
+template <class Csr, class Dense, class Stats>
+Dense run(const Csr& A, const Dense& X, const Dense& Y, const fmm_opspec& c, int t, Stats* stats) {
+    check_dims(A, X, Y);
+    if (t < 1) throw std::invalid_argument("fused_mm: t must be >= 1");
+    Dense Z(A.nrows, X.dim);
+    fmm_stats st{};
+    if (A.nrows > 0) {
+        Context& ctx = Context::for_shards(t);
+        fmm_graph* g = ctx.graph_for(A);
+        const float* y = (&X == &Y) ? X.data.data() : Y.data.data();
+        throw_status(fmm_run(ctx.get(), g, &c, X.dim, X.data.data(), Y.nrows, y, Z.data.data(),
+                             FMM_HOST_PTRS, &st),
+                     ctx.get());
+    } else {
+        int32_t pat = FMM_PATTERN_GENERIC;
+        fmm_pattern_of(&c, &pat);
+        st.pattern = pat;
+        st.threads = t;
+    }
+    if (stats) {
+        stats->aux_bytes = static_cast<decltype(stats->aux_bytes)>(st.aux_bytes);
+        stats->threads = st.threads;
+        // device-only patterns are GENERIC in the reference's enum
+        const int p = st.pattern <= FMM_PATTERN_GENERIC ? st.pattern : FMM_PATTERN_GENERIC;
+        stats->pattern = static_cast<decltype(stats->pattern)>(p);
+    }
+    return Z;
+}
+
+struct NoStats {
+    std::size_t aux_bytes;
+    int threads;
+    int pattern;
+};
+
+}  // namespace detail
+
+// Drop-in for fusedmm::fused_mm<float> (kernel.hpp:297-353).
+template <class Csr, class Dense, class Spec, class Stats = detail::NoStats,
+          class Opts = types::KernelOptions>
+Dense fused_mm(const Csr& A, const Dense& X, const Dense& Y, const Spec& spec, int t,
+               Stats* stats = nullptr, const Opts& opts = {}) {
+    (void)opts;  // lane_width is a CPU blocking width; the device shape is chosen by d
+    const bool user = static_cast<int>(spec.vop) == FMM_VOP_USER ||
+                      static_cast<int>(spec.rop) == FMM_ROP_USER ||
+                      static_cast<int>(spec.sop) == FMM_SOP_USER ||
+                      static_cast<int>(spec.mop) == FMM_MOP_USER ||
+                      static_cast<int>(spec.aop) == FMM_AOP_USER;
+    if (user) {
+        detail::check_dims(A, X, Y);
+        throw unsupported("fused_mm: USER slot has no device kernel (use a device op descriptor)");
+    }
+    return detail::run(A, X, Y, detail::to_c(spec), t, stats);
+}
+
+// Overload taking the device op descriptor (configs 3/4: tdist_ops(),
+// fr_attract_ops(k)), since a std::function cannot be introspected.
+template <class Csr, class Dense, class Stats = detail::NoStats>
+Dense fused_mm(const Csr& A, const Dense& X, const Dense& Y, const fmm_opspec& ops, int t,
+               Stats* stats = nullptr) {
+    return detail::run(A, X, Y, ops, t, stats);
+}
+
+}  // namespace cuda
+}  // namespace fusedmm

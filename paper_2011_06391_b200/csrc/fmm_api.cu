@@ -12,6 +12,7 @@
 #include "fmm_plan.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -42,6 +43,7 @@ struct Shard {
 
 struct fmm_ctx {
     std::vector<Shard> shards;
+    int variant = -1;  // kernel shape variant (FMM_VARIANT env, tuning only)
     std::string err;
     std::mutex mu;
 };
@@ -51,7 +53,7 @@ namespace {
 struct GShard {
     int shard = 0;
     int64_t row_begin = 0, row_end = 0, nnz = 0;
-    int64_t n_split_rows = 0, n_chunks = 0, n_slots = 0, nonempty = 0, max_degree = 0;
+    int64_t n_split_rows = 0, n_wide_rows = 0, n_chunks = 0, n_slots = 0, nonempty = 0, max_degree = 0;
     int64_t* row_ptr = nullptr;
     int32_t* col = nullptr;
     float* val = nullptr;
@@ -156,15 +158,15 @@ bool default_exact(int pattern, int64_t d) {
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
 bool launch_rows(const fmm::KParams& p, int pattern, int d, bool exact, bool a16, bool a8,
-                 cudaStream_t s) {
+                 int variant, cudaStream_t s) {
     const bool vec = fmm::aligned_shape(d, a16, a8);
     if (vec) {
         switch (pattern) {
-            case FMM_PATTERN_SIGMOID_EMBED: return fmm::launch_sigmoid(p, d, exact, s);
-            case FMM_PATTERN_SPMM_GCN: return fmm::launch_gcn(p, d, exact, s);
-            case FMM_PATTERN_FR_LAYOUT: return fmm::launch_fr(p, d, exact, s);
-            case FMM_PATTERN_TDIST: return fmm::launch_tdist(p, d, exact, s);
-            case FMM_PATTERN_FR_ATTRACT: return fmm::launch_frattr(p, d, exact, s);
+            case FMM_PATTERN_SIGMOID_EMBED: return fmm::launch_sigmoid(p, d, exact, variant, s);
+            case FMM_PATTERN_SPMM_GCN: return fmm::launch_gcn(p, d, exact, variant, s);
+            case FMM_PATTERN_FR_LAYOUT: return fmm::launch_fr(p, d, exact, variant, s);
+            case FMM_PATTERN_TDIST: return fmm::launch_tdist(p, d, exact, variant, s);
+            case FMM_PATTERN_FR_ATTRACT: return fmm::launch_frattr(p, d, exact, variant, s);
             default: break;
         }
     }
@@ -175,7 +177,7 @@ bool launch_rows(const fmm::KParams& p, int pattern, int d, bool exact, bool a16
 // Returns the number of kernels launched, or -1 if no instantiation fits.
 int launch_shard(const GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, bool exact,
                  const float* X, int64_t row0, const float* Y, float* Z, float* partial,
-                 const float* val, cudaStream_t stream) {
+                 const float* val, int variant, cudaStream_t stream) {
     fmm::KParams p{};
     p.row_ptr = gs.row_ptr;
     p.col = gs.col;
@@ -192,24 +194,28 @@ int launch_shard(const GShard& gs, const fmm_opspec& spec, int pattern, int64_t 
     p.k = spec.k;
     const int64_t rows = gs.row_end - gs.row_begin;
     const bool split = !exact && gs.n_chunks > 0;
-    if (split) {
+    if (!exact) {
+        // fast scheme: chunks of split rows, then wide rows, then narrow rows
         p.chunks = gs.chunks;
         p.n_chunk_items = gs.n_chunks;
         p.order = gs.order + gs.n_split_rows;
-        p.n_row_items = rows - gs.n_split_rows;
+        p.n_wide_rows = gs.n_wide_rows;
+        p.n_narrow_rows = rows - gs.n_split_rows - gs.n_wide_rows;
     } else {
+        // exact scheme: every row folded by one lane group, storage order
         p.chunks = nullptr;
         p.n_chunk_items = 0;
         p.order = gs.order;
-        p.n_row_items = rows;
+        p.n_wide_rows = 0;
+        p.n_narrow_rows = rows;
     }
-    if (p.n_chunk_items + p.n_row_items == 0) return 0;
+    if (p.n_chunk_items + p.n_wide_rows + p.n_narrow_rows == 0) return 0;
     const size_t a = static_cast<size_t>(d) * sizeof(float);
     const bool a16 = (d % 4 == 0) && aligned(X, 16) && aligned(Y, 16) && aligned(Z, 16) &&
                      (partial == nullptr || aligned(partial, 16)) && (a % 16 == 0);
     const bool a8 = (d % 2 == 0) && aligned(X, 8) && aligned(Y, 8) && aligned(Z, 8) &&
                     (partial == nullptr || aligned(partial, 8));
-    if (!launch_rows(p, pattern, static_cast<int>(d), exact, a16, a8, stream)) return -1;
+    if (!launch_rows(p, pattern, static_cast<int>(d), exact, a16, a8, variant, stream)) return -1;
     int launches = 1;
     if (split && gs.n_split_rows > 0) {
         fmm::fmm_combine_kernel<<<static_cast<unsigned>(gs.n_split_rows), 256, 0, stream>>>(
@@ -270,6 +276,7 @@ fmm_status fmm_create(int ngpu, const int* devs, fmm_ctx** out) {
     fmm_ctx* ctx = new (std::nothrow) fmm_ctx();
     if (!ctx) return FMM_E_OOM;
     ctx->shards.resize(ngpu);
+    if (const char* v = std::getenv("FMM_VARIANT")) ctx->variant = std::atoi(v);
     for (int i = 0; i < ngpu; ++i) {
         const int dev = devs ? devs[i] : (i % ndev);
         if (dev < 0 || dev >= ndev) {
@@ -404,6 +411,7 @@ fmm_status fmm_graph_upload(fmm_ctx* ctx, int64_t m, int64_t n, const int64_t* r
         }
         gs.nnz = P.nnz;
         gs.n_split_rows = P.n_split_rows;
+        gs.n_wide_rows = P.n_wide_rows;
         gs.n_chunks = static_cast<int64_t>(P.chunks.size());
         gs.n_slots = P.n_slots;
         gs.nonempty = P.nonempty_rows;
@@ -570,7 +578,7 @@ fmm_status fmm_run(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec, int
             aux = std::max(aux, pb);
         }
         if (timed) FMM_CK(ctx, cudaEventRecord(sh.ev_k0, stream));
-        const int l = launch_shard(gs, *spec, pattern, d, exact, xd, row0, yd, zd, part, gs.val, stream);
+        const int l = launch_shard(gs, *spec, pattern, d, exact, xd, row0, yd, zd, part, gs.val, ctx->variant, stream);
         if (l < 0) return set_err(ctx, FMM_E_UNSUPPORTED, "fused_mm: no kernel for this d / alignment");
         launches += l;
         FMM_CK(ctx, cudaGetLastError());
@@ -658,7 +666,7 @@ fmm_status fmm_iterate(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec,
             float* xn = static_cast<float*>(cur == 0 ? sh.Xb.ptr : sh.Y.ptr);
             const int l = launch_shard(gs, *spec, pattern, d, exact, xc, gs.row_begin, xc,
                                        xn + gs.row_begin * d, static_cast<float*>(sh.partial.ptr),
-                                       gs.val, sh.stream());
+                                       gs.val, ctx->variant, sh.stream());
             if (l < 0) return set_err(ctx, FMM_E_UNSUPPORTED, "iterate: no kernel for this d / alignment");
             launches += l;
             FMM_CK(ctx, cudaGetLastError());

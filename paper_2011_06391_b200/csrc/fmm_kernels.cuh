@@ -39,10 +39,11 @@ struct KParams {
     const float* Y;          // y_v = Y + v * d
     float* Z;                // z_r = Z + r * d   (r shard-local)
     float* partial;          // chunk partial rows: partial + slot * d
-    const int32_t* order;    // row items (shard-local rows)
+    const int32_t* order;    // rows, heavy first: wide rows then narrow rows
     const int4* chunks;      // chunk items {row, k, slot, 0}
     int64_t n_chunk_items;
-    int64_t n_row_items;
+    int64_t n_wide_rows;     // rows a whole warp folds (edges over its groups)
+    int64_t n_narrow_rows;   // rows one lane group folds
     int64_t row0;
     int chunk;               // edges per chunk (fast scheme)
     int d;
@@ -209,180 +210,288 @@ __device__ __forceinline__ float group_prod(float v) {
 }
 
 // --------------------------------------------------------------- the kernel
-// Template shape: lane group of LPR lanes, each lane holding NV vectors of
-// VEC floats: element j = (i*LPR + lane)*VEC + c. MASKED kernels (VEC == 1)
-// serve any d <= 32*NV with lanes past d idle.
-template <class Ops, int LPR, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED>
+// Per-edge work for U gathered neighbour rows: ROP across the group, SOP,
+// MOP, AOP into z (update_u's loop body, kernel.hpp:92-106).
+template <class Ops, int LPG, int VEC, int NV, int U, bool EXACT, bool MASKED>
+__device__ __forceinline__ void consume_edges(const Ops& ops, const KParams& p, const float (&x)[NV * VEC],
+                                              float (&z)[NV * VEC], const float (&y)[U][NV * VEC],
+                                              const float (&a)[U], const bool (&ok)[U],
+                                              const bool (&elem_ok)[NV]) {
+    constexpr int NE = NV * VEC;
+    // ASUM accumulations may run predicated (an invalid edge adds +0);
+    // AMAX and the exact scheme skip invalid edges explicitly.
+    const bool predicated = !EXACT && ops.aop() == FMM_AOP_ASUM;
+    if (ops.rop() != FMM_ROP_NOOP) {
+        const bool prod = rop_is_product(ops.rop());
+        float s[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            float acc = prod ? 1.0f : 0.0f;
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                if (!elem_ok[i]) continue;
+#pragma unroll
+                for (int c = 0; c < VEC; ++c)
+                    acc = vop_rop_step<EXACT>(ops, acc, x[i * VEC + c], y[u][i * VEC + c]);
+            }
+            s[u] = acc;
+        }
+        if (LPG > 1) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) s[u] = prod ? group_prod<LPG>(s[u]) : group_sum<LPG>(s[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            float sv = s[u];
+            if (ops.rop() == FMM_ROP_NORM) sv = sqrtf(sv);
+            float h = sop_apply(ops, sv, p.alpha, p.k);
+            if (predicated) {
+                h = ok[u] ? h : 0.0f;
+            } else if (!ok[u]) {
+                continue;
+            }
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+                float w;
+                if (ops.mop() == FMM_MOP_SEL2ND) {
+                    w = y[u][e];
+                } else if (ops.mop() == FMM_MOP_MUL_VOP) {
+                    const float t = vop_apply<EXACT>(ops, x[e], y[u][e]);
+                    if (ops.aop() == FMM_AOP_ASUM && !EXACT) {
+                        z[e] = fmaf(a[u] * h, t, z[e]);
+                        continue;
+                    }
+                    w = fmul<EXACT>(a[u], fmul<EXACT>(h, t));
+                } else {  // MUL: h * y_v, a_uv ignored (ops.hpp:131-137)
+                    if (ops.aop() == FMM_AOP_ASUM) {
+                        z[e] = fmac<EXACT>(z[e], h, y[u][e]);
+                        continue;
+                    }
+                    w = fmul<EXACT>(h, y[u][e]);
+                }
+                z[e] = aop_apply<EXACT>(ops, z[e], w);
+            }
+        }
+    } else {
+        // vector message: SOP elementwise, MOP with a_uv (ops.hpp:123-127, 150-156)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (!ok[u]) continue;
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+                float t = vop_apply<EXACT>(ops, x[e], y[u][e]);
+                t = sop_apply(ops, t, p.alpha, p.k);
+                float w;
+                if (ops.mop() == FMM_MOP_SEL2ND) {
+                    w = y[u][e];
+                } else {
+                    if (ops.aop() == FMM_AOP_ASUM) {
+                        z[e] = fmac<EXACT>(z[e], a[u], t);
+                        continue;
+                    }
+                    w = fmul<EXACT>(a[u], t);
+                }
+                z[e] = aop_apply<EXACT>(ops, z[e], w);
+            }
+        }
+    }
+}
+
+template <int LPG, int VEC, int NV, int U, bool MASKED>
+__device__ __forceinline__ void gather_rows(const float* __restrict__ Y, int d, const int (&v)[U],
+                                            const bool (&ok)[U], const bool (&elem_ok)[NV], int gl,
+                                            float (&y)[U][NV * VEC]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const float* yr = Y + static_cast<int64_t>(v[u]) * d;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            if (ok[u] && elem_ok[i]) {
+                load_vec<VEC>(&y[u][i * VEC], yr + (i * LPG + gl) * VEC);
+            } else {
+#pragma unroll
+                for (int c = 0; c < VEC; ++c) y[u][i * VEC + c] = 0.0f;
+            }
+        }
+    }
+}
+
+// Work items, in launch order (heaviest first, LPT-like):
+//   [0, n_chunk_items)                 chunk of a split row  -> wide warp
+//   [.., + n_wide_rows)                row order[i]          -> wide warp
+//   then narrow rows, GPW = 32/LPG per warp, one per lane group.
+// A wide warp spreads its item's edges over the GPW groups round-robin
+// (edge k -> group k % GPW), each group folds its edges in storage order,
+// and the GPW partial z are combined by an xor-butterfly in fixed order.
+// Lane layout: element j = (i*LPG + lane_in_group)*VEC + c.
+template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED>
 __global__ void __launch_bounds__(256)
 fmm_rows_kernel(const KParams p, const Ops ops) {
     constexpr int NE = NV * VEC;
-    constexpr int B = (LPR > UNROLL) ? LPR : UNROLL;  // edges per batch
-    constexpr int KPL = B / LPR;                       // column slots per lane
-    static_assert(B % LPR == 0 && B % UNROLL == 0, "batch shape");
+    constexpr int GPW = 32 / LPG;
+    constexpr int U = UNROLL;
+    static_assert(32 % LPG == 0, "group shape");
 
     const int lane = threadIdx.x & 31;
-    const int gl = lane & (LPR - 1);
-    const int gbase = lane & ~(LPR - 1);
-    const int64_t gid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / LPR;
-    const int64_t total = p.n_chunk_items + p.n_row_items;
-    const bool active = gid < total;
-    if (__all_sync(0xffffffffu, !active)) return;
-
-    const int d = MASKED ? p.d : LPR * VEC * NV;
-    const bool scalar_msg = ops.rop() != FMM_ROP_NOOP;
-    const bool need_x = ops.vop() != FMM_VOP_SEL2ND;
-    const bool has_val = p.val != nullptr;
+    const int gl = lane & (LPG - 1);
+    const int g = lane / LPG;
+    const int gbase = lane & ~(LPG - 1);
+    const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t n_wide_items = EXACT ? 0 : p.n_chunk_items + p.n_wide_rows;
+    const bool wide = warp < n_wide_items;  // warp-uniform
 
     int64_t r = 0, e0 = 0, e1 = 0;
     float* out = nullptr;
-    if (active) {
-        if (gid < p.n_chunk_items) {
-            const int4 c = p.chunks[gid];
+    bool active;
+    if (wide) {
+        active = true;
+        if (warp < p.n_chunk_items) {
+            const int4 c = p.chunks[warp];
             r = c.x;
-            const int64_t rb = p.row_ptr[r], re = p.row_ptr[r + 1];
-            e0 = rb + static_cast<int64_t>(c.y) * p.chunk;
-            e1 = min(e0 + static_cast<int64_t>(p.chunk), re);
-            out = p.partial + static_cast<int64_t>(c.z) * d;
+            e0 = p.row_ptr[r] + static_cast<int64_t>(c.y) * p.chunk;
+            e1 = min(e0 + static_cast<int64_t>(p.chunk), p.row_ptr[r + 1]);
+            out = p.partial + static_cast<int64_t>(c.z) * (MASKED ? p.d : LPG * VEC * NV);
         } else {
-            r = p.order[gid - p.n_chunk_items];
+            r = p.order[warp - p.n_chunk_items];
             e0 = p.row_ptr[r];
             e1 = p.row_ptr[r + 1];
-            out = p.Z + r * d;
+            out = p.Z + r * (MASKED ? p.d : LPG * VEC * NV);
+        }
+    } else {
+        const int64_t idx = (warp - n_wide_items) * GPW + g;
+        active = idx < p.n_narrow_rows;
+        if (__all_sync(0xffffffffu, !active)) return;
+        if (active) {
+            r = p.order[p.n_wide_rows + idx];
+            e0 = p.row_ptr[r];
+            e1 = p.row_ptr[r + 1];
+            out = p.Z + r * (MASKED ? p.d : LPG * VEC * NV);
         }
     }
-    const int n = static_cast<int>(e1 - e0);
-    const int nmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(n)));
 
-    // x_u and z_u in registers
+    const int d = MASKED ? p.d : LPG * VEC * NV;
+    const bool need_x = ops.vop() != FMM_VOP_SEL2ND;
+    const bool has_val = p.val != nullptr;
+
     float x[NE], z[NE];
     const float ident = aop_identity(ops);
 #pragma unroll
     for (int i = 0; i < NE; ++i) { x[i] = 0.0f; z[i] = ident; }
     bool elem_ok[NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) elem_ok[i] = !MASKED || ((i * LPR + gl) * VEC < d);
+    for (int i = 0; i < NV; ++i) elem_ok[i] = !MASKED || ((i * LPG + gl) * VEC < d);
     if (active && need_x) {
         const float* xr = p.X + (p.row0 + r) * d;
 #pragma unroll
         for (int i = 0; i < NV; ++i)
-            if (elem_ok[i]) load_vec<VEC>(&x[i * VEC], xr + (i * LPR + gl) * VEC);
+            if (elem_ok[i]) load_vec<VEC>(&x[i * VEC], xr + (i * LPG + gl) * VEC);
     }
 
-    for (int base = 0; base < nmax; base += B) {
-        // column indices (and a_uv) of this batch: edge b lives in lane b % LPR, slot b / LPR
-        int cidx[KPL];
-        float aval[KPL];
+    if (wide) {
+        // ---- one item per warp; edge k of the item goes to group k % GPW
+        constexpr int SB = GPW * U;                   // edges per sub-batch
+        constexpr int B = SB > 32 ? SB : 32;          // edges per column batch
+        constexpr int KPL = B / 32;                   // column slots per lane
+        static_assert(SB <= 32 ? (32 % SB == 0) : (SB % 32 == 0), "sub-batch shape");
+        const int n = static_cast<int>(e1 - e0);
+        for (int base = 0; base < n; base += B) {
+            int cidx[KPL];
+            float aval[KPL];
 #pragma unroll
-        for (int q = 0; q < KPL; ++q) {
-            const int eb = base + q * LPR + gl;
-            cidx[q] = 0;
-            aval[q] = 1.0f;
-            if (eb < n) {
-                cidx[q] = ld_stream_i32(p.col + e0 + eb);
-                if (has_val) aval[q] = ld_stream_f32(p.val + e0 + eb);
+            for (int q = 0; q < KPL; ++q) {
+                const int eb = base + q * 32 + lane;
+                cidx[q] = 0;
+                aval[q] = 1.0f;
+                if (eb < n) {
+                    cidx[q] = ld_stream_i32(p.col + e0 + eb);
+                    if (has_val) aval[q] = ld_stream_f32(p.val + e0 + eb);
+                }
             }
-        }
-        const int cnt = min(B, nmax - base);  // warp-uniform
-        // B == UNROLL: one sub-batch (unrolled, static slot indices).
-        // B > UNROLL only when LPR > UNROLL, i.e. one column slot per lane.
+            const int cnt = min(B, n - base);
+            // SB >= 32: a single sub-batch per column batch (static slots);
+            // SB < 32: KPL == 1 and the sub-batch offset s is a run-time value.
 #pragma unroll 1
-        for (int u0 = 0; u0 < B; u0 += UNROLL) {
-            if (u0 >= cnt) break;
-            float y[UNROLL][NE];
-            float a[UNROLL];
-            bool ok[UNROLL];
+            for (int s = 0; s < B; s += SB) {
+                if (s >= cnt) break;
+                int v[U];
+                float a[U];
+                bool ok[U];
 #pragma unroll
-            for (int u = 0; u < UNROLL; ++u) {
-                const int b = u0 + u;
-                const int v = __shfl_sync(0xffffffffu, cidx[KPL == 1 ? 0 : b / LPR], gbase + (b % LPR));
-                a[u] = has_val ? __shfl_sync(0xffffffffu, aval[KPL == 1 ? 0 : b / LPR], gbase + (b % LPR)) : 1.0f;
-                ok[u] = (base + b) < n;
-                const float* yr = p.Y + static_cast<int64_t>(v) * d;
-#pragma unroll
-                for (int i = 0; i < NV; ++i) {
-                    if (ok[u] && elem_ok[i]) {
-                        load_vec<VEC>(&y[u][i * VEC], yr + (i * LPR + gl) * VEC);
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < VEC; ++c) y[u][i * VEC + c] = 0.0f;
-                    }
+                for (int u = 0; u < U; ++u) {
+                    const int bq = s + u * GPW;
+                    const int slot = KPL == 1 ? 0 : (u * GPW) / 32;
+                    const int src = (bq % 32) + g;
+                    v[u] = __shfl_sync(0xffffffffu, cidx[slot], src);
+                    a[u] = has_val ? __shfl_sync(0xffffffffu, aval[slot], src) : 1.0f;
+                    ok[u] = (base + bq + g) < n;
                 }
+                float y[U][NE];
+                gather_rows<LPG, VEC, NV, U, MASKED>(p.Y, d, v, ok, elem_ok, gl, y);
+                consume_edges<Ops, LPG, VEC, NV, U, EXACT, MASKED>(ops, p, x, z, y, a, ok, elem_ok);
             }
-            if (scalar_msg) {
-                // ROP per edge: lane-local partial, then butterfly across the group
-                const bool prod = rop_is_product(ops.rop());
-                float s[UNROLL];
+        }
+        // fold the GPW group partials (fixed butterfly order -> deterministic)
+        if (GPW > 1) {
+            const bool is_max = ops.aop() == FMM_AOP_AMAX;
 #pragma unroll
-                for (int u = 0; u < UNROLL; ++u) {
-                    float acc = prod ? 1.0f : 0.0f;
+            for (int off = LPG; off < 32; off <<= 1) {
 #pragma unroll
-                    for (int i = 0; i < NV; ++i) {
-                        if (!elem_ok[i]) continue;
-#pragma unroll
-                        for (int c = 0; c < VEC; ++c)
-                            acc = vop_rop_step<EXACT>(ops, acc, x[i * VEC + c], y[u][i * VEC + c]);
-                    }
-                    s[u] = acc;
-                }
-                if (LPR > 1) {
-#pragma unroll
-                    for (int u = 0; u < UNROLL; ++u)
-                        s[u] = prod ? group_prod<LPR>(s[u]) : group_sum<LPR>(s[u]);
-                }
-#pragma unroll
-                for (int u = 0; u < UNROLL; ++u) {
-                    float sv = s[u];
-                    if (ops.rop() == FMM_ROP_NORM) sv = sqrtf(sv);
-                    const float h = sop_apply(ops, sv, p.alpha, p.k);
-                    if (!ok[u]) continue;
-#pragma unroll
-                    for (int e = 0; e < NE; ++e) {
-                        float w;
-                        if (ops.mop() == FMM_MOP_SEL2ND) {
-                            w = y[u][e];
-                        } else if (ops.mop() == FMM_MOP_MUL_VOP) {
-                            const float t = vop_apply<EXACT>(ops, x[e], y[u][e]);
-                            w = fmul<EXACT>(a[u], fmul<EXACT>(h, t));
-                        } else {  // MUL: h * y_v, a_uv ignored (ops.hpp:131-137)
-                            if (ops.aop() == FMM_AOP_ASUM) {
-                                z[e] = fmac<EXACT>(z[e], h, y[u][e]);
-                                continue;
-                            }
-                            w = fmul<EXACT>(h, y[u][e]);
-                        }
-                        z[e] = aop_apply<EXACT>(ops, z[e], w);
-                    }
-                }
-            } else {
-                // vector message: SOP elementwise, MOP with a_uv (ops.hpp:123-127, 150-156)
-#pragma unroll
-                for (int u = 0; u < UNROLL; ++u) {
-                    if (!ok[u]) continue;
-#pragma unroll
-                    for (int e = 0; e < NE; ++e) {
-                        float t = vop_apply<EXACT>(ops, x[e], y[u][e]);
-                        t = sop_apply(ops, t, p.alpha, p.k);
-                        float w;
-                        if (ops.mop() == FMM_MOP_SEL2ND) {
-                            w = y[u][e];
-                        } else {
-                            if (ops.aop() == FMM_AOP_ASUM) {
-                                z[e] = fmac<EXACT>(z[e], a[u], t);
-                                continue;
-                            }
-                            w = fmul<EXACT>(a[u], t);
-                        }
-                        z[e] = aop_apply<EXACT>(ops, z[e], w);
-                    }
+                for (int e = 0; e < NE; ++e) {
+                    const float o = __shfl_xor_sync(0xffffffffu, z[e], off);
+                    z[e] = is_max ? ((z[e] < o) ? o : z[e]) : z[e] + o;
                 }
             }
         }
-    }
-
-    if (active) {
+        // group gg stores vectors i with i % GPW == gg
 #pragma unroll
         for (int i = 0; i < NV; ++i)
-            if (elem_ok[i]) store_vec<VEC>(out + (i * LPR + gl) * VEC, &z[i * VEC]);
+            if ((i % GPW) == g && elem_ok[i]) store_vec<VEC>(out + (i * LPG + gl) * VEC, &z[i * VEC]);
+        return;
+    }
+
+    // ---- narrow: one row per lane group
+    {
+        constexpr int B = (LPG > U) ? LPG : U;  // edges per column batch
+        constexpr int KPL = B / LPG;            // column slots per lane
+        const int n = static_cast<int>(e1 - e0);
+        const int nmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(n)));
+        for (int base = 0; base < nmax; base += B) {
+            int cidx[KPL];
+            float aval[KPL];
+#pragma unroll
+            for (int q = 0; q < KPL; ++q) {
+                const int eb = base + q * LPG + gl;
+                cidx[q] = 0;
+                aval[q] = 1.0f;
+                if (eb < n) {
+                    cidx[q] = ld_stream_i32(p.col + e0 + eb);
+                    if (has_val) aval[q] = ld_stream_f32(p.val + e0 + eb);
+                }
+            }
+            const int cnt = min(B, nmax - base);  // warp-uniform
+#pragma unroll 1
+            for (int u0 = 0; u0 < B; u0 += U) {
+                if (u0 >= cnt) break;
+                int v[U];
+                float a[U];
+                bool ok[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int b = u0 + u;
+                    v[u] = __shfl_sync(0xffffffffu, cidx[KPL == 1 ? 0 : b / LPG], gbase + (b % LPG));
+                    a[u] = has_val ? __shfl_sync(0xffffffffu, aval[KPL == 1 ? 0 : b / LPG], gbase + (b % LPG)) : 1.0f;
+                    ok[u] = (base + b) < n;
+                }
+                float y[U][NE];
+                gather_rows<LPG, VEC, NV, U, MASKED>(p.Y, d, v, ok, elem_ok, gl, y);
+                consume_edges<Ops, LPG, VEC, NV, U, EXACT, MASKED>(ops, p, x, z, y, a, ok, elem_ok);
+            }
+        }
+        if (active) {
+#pragma unroll
+            for (int i = 0; i < NV; ++i)
+                if (elem_ok[i]) store_vec<VEC>(out + (i * LPG + gl) * VEC, &z[i * VEC]);
+        }
     }
 }
 

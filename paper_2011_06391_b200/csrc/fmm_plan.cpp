@@ -72,6 +72,7 @@ ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t ro
         if (deg > 0) ++P.nonempty_rows;
         P.max_degree = std::max(P.max_degree, deg);
         if (deg > kChunkEdges) ++P.n_split_rows;
+        else if (deg >= kWideMin) ++P.n_wide_rows;
         ++count[key_of(r) + 1];
     }
     for (int k = 0; k < kKeys; ++k) count[k + 1] += count[k];

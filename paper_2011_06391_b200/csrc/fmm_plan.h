@@ -15,6 +15,9 @@ namespace fmm {
 // Chunk boundaries sit at fixed row-relative offsets, so results do not
 // depend on the shard count.
 constexpr int kChunkEdges = 256;
+// Unsplit rows at least this long are folded by a whole warp on the fast
+// scheme (a bucket boundary, so they form a prefix of the ordered rows).
+constexpr int kWideMin = 64;
 
 struct Int4 {
     int32_t x, y, z, w;
@@ -40,6 +43,7 @@ struct ShardPlan {
     // bucket so light rows keep their memory locality.
     std::vector<int32_t> order;
     int64_t n_split_rows = 0;             // prefix of `order` cut into chunks
+    int64_t n_wide_rows = 0;              // next rows with degree >= kWideMin
     std::vector<Int4> chunks;             // {row, k, slot, 0}
     std::vector<Int4> split_rows;         // {row, first slot, nchunks, 0}
     int64_t n_slots = 0;

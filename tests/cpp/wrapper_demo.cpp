@@ -1,0 +1,70 @@
+// Exercise include/fusedmm_cuda.hpp the way reference host code would:
+// the reference's own KATs (proj/tests/test_kernel.cpp:110-144) through the
+// drop-in fusedmm::cuda::fused_mm. Built on any box; run on a GPU box.
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+
+#include "fusedmm_cuda.hpp"
+
+using namespace fusedmm::cuda::types;
+namespace fc = fusedmm::cuda;
+
+static int failures = 0;
+#define CHECK(c) do { if (!(c)) { std::printf("FAIL %s:%d %s\n", __FILE__, __LINE__, #c); ++failures; } } while (0)
+
+int main() {
+    // GCN tiny case: {5,5,6,6} (test_kernel.cpp:110-116)
+    CsrMatrix A;
+    A.nrows = 2; A.ncols = 2;
+    A.row_ptr = {0, 2, 3};
+    A.col_idx = {0, 1, 1};
+    A.values = {1.f, 2.f, 3.f};
+    DenseMatrix Y(2, 2);
+    Y.data = {1, 1, 2, 2};
+    DenseMatrix X(2, 2);
+    OpSpec gcn{Vop::SEL2ND, Rop::NOOP, Sop::NOOP, Mop::MUL, Aop::ASUM};
+    KernelStats st;
+    DenseMatrix Z = fc::fused_mm(A, X, Y, gcn, 2, &st);
+    CHECK(Z.data == (std::vector<float>{5, 5, 6, 6}));
+    CHECK(st.threads == 2 && st.pattern == KnownPattern::SPMM_GCN);
+
+    // sigmoid 2-cycle: 1.0 and 0.5 (test_kernel.cpp:118-125)
+    CsrMatrix C;
+    C.nrows = 2; C.ncols = 2;
+    C.row_ptr = {0, 1, 2};
+    C.col_idx = {1, 0};
+    C.values = {1.f, 1.f};
+    DenseMatrix X1(2, 1), Y1(2, 1);
+    Y1.data = {1, 2};
+    OpSpec emb{Vop::MUL, Rop::RSUM, Sop::SIGMOID, Mop::MUL, Aop::ASUM};
+    DenseMatrix Z1 = fc::fused_mm(C, X1, Y1, emb, 1);
+    CHECK(std::fabs(Z1.data[0] - 1.f) < 1e-6f && std::fabs(Z1.data[1] - 0.5f) < 1e-6f);
+
+    // dimension mismatch throws std::invalid_argument (test_kernel.cpp:134-144)
+    DenseMatrix Xbad(1, 2);
+    bool threw = false;
+    try { fc::fused_mm(A, Xbad, Y, gcn, 1); } catch (const std::invalid_argument&) { threw = true; }
+    CHECK(threw);
+    threw = false;
+    try { fc::fused_mm(A, X, Y, gcn, 0); } catch (const std::invalid_argument&) { threw = true; }
+    CHECK(threw);
+    // USER slot: no device kernel, no CPU fallback
+    OpSpec user = emb;
+    user.vop = Vop::USER;
+    threw = false;
+    try { fc::fused_mm(A, X, Y, user, 1); } catch (const fc::unsupported&) { threw = true; }
+    CHECK(threw);
+    // t-distribution through the device op descriptor: t=(-2,-2), h=1/9
+    CsrMatrix E;
+    E.nrows = 1; E.ncols = 1;
+    E.row_ptr = {0, 1};
+    E.col_idx = {0};
+    DenseMatrix Xe(1, 2), Ye(1, 2);
+    Xe.data = {1, 2};
+    Ye.data = {3, 4};
+    DenseMatrix Ze = fc::fused_mm(E, Xe, Ye, fc::tdist_ops(), 1);
+    CHECK(std::fabs(Ze.data[0] + 2.f / 9.f) < 1e-6f);
+    std::printf("%s (%d failures)\n", failures ? "FAILED" : "wrapper ok", failures);
+    return failures ? 1 : 0;
+}

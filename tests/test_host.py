@@ -1,0 +1,124 @@
+"""CPU: host-side logic — containers (matrix.hpp), the seeded input
+generators against the reference generator and the survey's probe numbers,
+and the byte model the roofline uses."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2011_06391_b200 import configs
+from paper_2011_06391_b200 import fusedmm as F
+
+
+# ----------------------------------------------------------- containers
+def test_csr_from_coo_dedup_first_occurrence_order():
+    # matrix.hpp:84-140: duplicates summed, storage order = first occurrence
+    A = F.csr_from_coo([(0, 2, 1.0), (0, 0, 2.0), (0, 2, 3.0), (1, 1, 1.0)], 2, 3)
+    assert A.row_ptr.tolist() == [0, 2, 3]
+    assert A.col_idx.tolist() == [2, 0, 1]
+    assert A.values.tolist() == [4.0, 2.0, 1.0]
+    with pytest.raises(F.InvalidArgument):
+        F.csr_from_coo([(0, 3, 1.0)], 2, 3)
+
+
+def test_csr_roundtrip_property():
+    # test_core.cpp:100-135
+    rng = np.random.default_rng(11)
+    for _ in range(30):
+        m, n = int(rng.integers(1, 20)), int(rng.integers(1, 20))
+        ent = [(int(rng.integers(0, m)), int(rng.integers(0, n)), float(rng.uniform(0.1, 2))) for _ in
+               range(int(rng.integers(0, m * n + 1)))]
+        A = F.csr_from_coo(ent, m, n)
+        assert F.validate(A) is None
+        exp = {}
+        for r, c, v in ent:
+            exp[(r, c)] = exp.get((r, c), 0.0) + v
+        got = {(r, int(A.col_idx[p])): float(A.values[p]) for r in range(m)
+               for p in range(A.row_ptr[r], A.row_ptr[r + 1])}
+        assert set(got) == set(exp)
+        for k in exp:
+            assert got[k] == pytest.approx(exp[k], rel=1e-5)
+
+
+def test_validate_and_stats():
+    A = F.CsrMatrix(2, 2, np.array([0, 2, 1]), np.array([0, 1]))
+    assert "monotone" in F.validate(A)
+    A = F.CsrMatrix(1, 2, np.array([0, 2]), np.array([1, 1]))
+    assert "duplicate" in F.validate(A)
+    A = F.csr_from_coo([(0, v, 1.0) for v in range(1, 6)], 6, 6)  # star (test_core.cpp:83-90)
+    s = F.stats(A)
+    assert s.max_degree == 5 and s.avg_degree == pytest.approx(5 / 6)
+    with pytest.raises(F.InvalidArgument):
+        F.DenseMatrix(1, 2, [1.0, np.nan])  # test_core.cpp:138-141
+
+
+# ----------------------------------------------------------- generators
+def test_generators_are_deterministic():
+    a = configs.config2(scale=10)
+    b = configs.config2(scale=10)
+    assert np.array_equal(a.A.col_idx, b.A.col_idx) and np.array_equal(a.X.data, b.X.data)
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 5])
+def test_rmat_postprocessing_properties(cfg):
+    w = configs.get(cfg, small=True)
+    A = w.A
+    rows = np.repeat(np.arange(A.nrows), np.diff(A.row_ptr))
+    assert not np.any(rows == A.col_idx)  # self-loops dropped
+    assert F.validate(A) is None  # sorted unique, in range
+    key = set(zip(rows.tolist(), A.col_idx.tolist()))
+    assert all((c, r) in key for r, c in key)  # symmetric
+    for u in range(0, A.nrows, max(1, A.nrows // 50)):
+        assert np.all(np.diff(A.row_cols(u)) > 0)
+
+
+def test_config1_recipe():
+    w = configs.config1(n=512)
+    A = w.A
+    assert np.all(np.diff(A.row_ptr) == 16)
+    for u in range(512):
+        c = A.row_cols(u)
+        assert np.all(np.diff(c) > 0)
+    assert A.values.min() >= 0 and A.values.max() < 1
+    assert w.X.data.min() >= -1 and w.X.data.max() < 1
+
+
+def test_config4_recipe():
+    w = configs.config4(side=32)
+    A = w.A
+    deg = np.diff(A.row_ptr)
+    assert deg.min() >= 2 and deg.max() <= 15
+    assert abs(w.X.array[5 * 32 + 7, 0] - 7) < 0.1 and abs(w.X.array[5 * 32 + 7, 1] - 5) < 0.1
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built here")
+def test_rmat_symmetrised_equals_reference_stream_postprocessed():
+    # our generator == reference rmat_generate (rmat.hpp:24-61) + BASELINE's
+    # post-processing (drop self-loops, symmetrise, dedup, sort)
+    rp, cl, _ = oracle.ref_rmat(11, 8, 99)
+    rows = np.repeat(np.arange(2048), np.diff(rp))
+    keep = rows != cl
+    r2 = np.concatenate([rows[keep], cl[keep]])
+    c2 = np.concatenate([cl[keep], rows[keep]])
+    key = np.unique(r2 * 2048 + c2)
+    A = configs.rmat_sym(11, 8, 99)
+    assert np.array_equal(A.col_idx, key % 2048)
+    assert np.array_equal(np.diff(A.row_ptr), np.bincount(key // 2048, minlength=2048))
+
+
+# ------------------------------------------------- pins at full size (survey)
+@pytest.mark.slow
+def test_full_size_graphs_match_survey_probe():
+    # SURVEY.md §8(d) [probe] numbers, produced with the reference generator
+    w1 = configs.config1()
+    assert w1.A.nnz() == 262144 and w1.alg_bytes() == 73_531_400
+    w2 = configs.config2()
+    deg = np.diff(w2.A.row_ptr)
+    assert w2.A.nnz() == 31_398_704 and int(deg.max()) == 64_782 and int((deg == 0).sum()) == 402_719
+    assert w2.alg_bytes() == 17_077_669_576
+    w3 = configs.config3(iters=1)
+    deg = np.diff(w3.A.row_ptr)
+    assert w3.A.nnz() == 32_417_756 and int(deg.max()) == 62_004 and int((deg == 0).sum()) == 1_048_972
+    assert w3.alg_bytes() == 4_698_523_512
+    w4 = configs.config4()
+    assert w4.A.nnz() == 25_157_628 and int(np.diff(w4.A.row_ptr).max()) == 15
+    assert w4.alg_bytes() == 402_554_840
