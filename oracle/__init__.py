@@ -152,6 +152,8 @@ class RefCall:
         self.h = prep(A.nrows, A.ncols, A.row_ptr.ctypes.data_as(P64), A.col_idx.ctypes.data_as(P64),
                       None if V is None else ptr(V), X.dim, ptr(Xa), Y.nrows, ptr(Ya),
                       C.byref(_spec(spec)), lane_width)
+        if not self.h:
+            raise ValueError("reference shim rejected the spec")
 
     def run(self, t: int | None = None, want_z: bool = True):
         L = ref_lib()

@@ -56,7 +56,8 @@ static void SFX(apply_aop)(int aop, REAL* acc, const REAL* w, int64_t d) {
 /* update_u, kernel.hpp:81-107. The MUL_VOP extension follows the USER-VOP
  * lambda route the reference needs for configs 3/4: the "VOP output" is
  * out_j = h * t_j with h = sop(rop(t)), the message is a vector, SOP is NOOP
- * and MOP=MUL gives w_j = a_uv * out_j (ops.hpp:150-156). */
+ * and MOP=MUL gives w_j = a_uv * out_j (ops.hpp:150-156). With ROP=NOOP there
+ * is no scalar to scale by and MUL_VOP acts as the vector-message MUL. */
 static void SFX(update_u)(const int64_t* cols, const REAL* vals, int64_t nk, const REAL* x_u,
                           const REAL* Y, int64_t d, const or_spec* sp, REAL* z_u, REAL* tmp,
                           REAL* w) {
@@ -66,7 +67,7 @@ static void SFX(update_u)(const int64_t* cols, const REAL* vals, int64_t nk, con
     for (k = 0; k < nk; ++k) {
         const REAL* y_v = Y + cols[k] * d;
         const REAL a = vals ? vals[k] : (REAL)1;
-        if (sp->mop == OR_MOP_MUL_VOP) {
+        if (sp->mop == OR_MOP_MUL_VOP && sp->rop != OR_ROP_NOOP) {
             REAL s, h;
             SFX(apply_vop)(sp->vop, x_u, y_v, tmp, d);
             s = SFX(apply_rop)(sp->rop, tmp, d);

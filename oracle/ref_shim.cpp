@@ -13,6 +13,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <stdexcept>
 #include <memory>
 #include <span>
 #include <vector>
@@ -40,6 +41,9 @@ template <typename T>
 OpSpec<T> make_ref_spec(const RefSpec& s) {
     OpSpec<T> spec;
     if (s.mop == EXT_MOP_MUL_VOP) {
+        if (s.vop != static_cast<int>(Vop::SUB) || s.rop != EXT_ROP_SQNORM ||
+            (s.sop != EXT_SOP_TDIST && s.sop != EXT_SOP_SQK) || s.aop != static_cast<int>(Aop::ASUM))
+            throw std::invalid_argument("ref_shim: only the config 3/4 lambdas use MUL_VOP");
         // USER VOP lambda: sq = sum (x_j - y_j)^2 sequentially, sc = sop(sq),
         // out_j = sc * (x_j - y_j)  (t-distribution: 1/(1+sq); FR: sq/k)
         const int sop = s.sop;
@@ -125,7 +129,11 @@ extern "C" {
 void* fmm_ref_prepare_f32(int64_t m, int64_t n, const int64_t* row_ptr, const int64_t* col,
                           const float* val, int64_t d, const float* X, int64_t ny, const float* Y,
                           const RefSpec* s, int lane_width) {
-    return prepare<float>(m, n, row_ptr, col, val, d, X, ny, Y, s, lane_width);
+    try {
+        return prepare<float>(m, n, row_ptr, col, val, d, X, ny, Y, s, lane_width);
+    } catch (const std::exception&) {
+        return nullptr;
+    }
 }
 int fmm_ref_run_f32(void* h, int t, float* Z, double* seconds) {
     return run(static_cast<Prepared<float>*>(h), t, Z, seconds);
@@ -135,7 +143,11 @@ void fmm_ref_release_f32(void* h) { delete static_cast<Prepared<float>*>(h); }
 void* fmm_ref_prepare_f64(int64_t m, int64_t n, const int64_t* row_ptr, const int64_t* col,
                           const double* val, int64_t d, const double* X, int64_t ny,
                           const double* Y, const RefSpec* s, int lane_width) {
-    return prepare<double>(m, n, row_ptr, col, val, d, X, ny, Y, s, lane_width);
+    try {
+        return prepare<double>(m, n, row_ptr, col, val, d, X, ny, Y, s, lane_width);
+    } catch (const std::exception&) {
+        return nullptr;
+    }
 }
 int fmm_ref_run_f64(void* h, int t, double* Z, double* seconds) {
     return run(static_cast<Prepared<double>*>(h), t, Z, seconds);
