@@ -131,13 +131,29 @@ __device__ __forceinline__ float vop_rop_step(const Ops& ops, float acc, float x
     return rop_step<EXACT>(ops, acc, vop_apply<EXACT>(ops, x, y));
 }
 
-// ops.hpp:53-56, 108-121 plus the device extensions TDIST / SQK
-template <class Ops>
+// 1/x for x >= 1 (x may be +inf): rcp.approx refined by one Newton step,
+// branch-free, within 1 ulp of the IEEE quotient.
+__device__ __forceinline__ float recip_ge1(float x) {
+    x = fminf(x, 3.0e38f);  // 1/inf -> 0 without a NaN from the Newton step
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return fmaf(r, fmaf(-x, r, 1.0f), r);
+}
+
+// ops.hpp:53-56, 108-121 plus the device extensions TDIST / SQK. Sigmoid is
+// 1/(1+exp(-s)) with CUDA's accurate expf (no LUT, no clamp);
+// the exact scheme divides with IEEE rounding, the fast one uses recip_ge1.
+template <bool EXACT, class Ops>
 __device__ __forceinline__ float sop_apply(const Ops& ops, float s, float alpha, float k) {
     switch (ops.sop()) {
-        case FMM_SOP_SIGMOID: return 1.0f / (1.0f + expf(-s));
+        case FMM_SOP_SIGMOID:
+            if constexpr (EXACT) return 1.0f / (1.0f + expf(-s));
+            else return recip_ge1(1.0f + expf(-s));
         case FMM_SOP_SCAL: return __fmul_rn(alpha, s);
-        case FMM_SOP_TDIST: return 1.0f / (1.0f + s);
+        case FMM_SOP_TDIST:
+            // s >= 0 after a squared / plain norm, so 1+s >= 1
+            if (!EXACT && (ops.rop() == FMM_ROP_SQNORM || ops.rop() == FMM_ROP_NORM)) return recip_ge1(1.0f + s);
+            return 1.0f / (1.0f + s);
         case FMM_SOP_SQK: return __fdiv_rn(s, k);
         default: return s;  // NOOP
     }
@@ -244,7 +260,7 @@ __device__ __forceinline__ void consume_edges(const Ops& ops, const KParams& p, 
         for (int u = 0; u < U; ++u) {
             float sv = s[u];
             if (ops.rop() == FMM_ROP_NORM) sv = sqrtf(sv);
-            float h = sop_apply(ops, sv, p.alpha, p.k);
+            float h = sop_apply<EXACT>(ops, sv, p.alpha, p.k);
             if (predicated) {
                 h = ok[u] ? h : 0.0f;
             } else if (!ok[u]) {
@@ -280,7 +296,7 @@ __device__ __forceinline__ void consume_edges(const Ops& ops, const KParams& p, 
 #pragma unroll
             for (int e = 0; e < NE; ++e) {
                 float t = vop_apply<EXACT>(ops, x[e], y[u][e]);
-                t = sop_apply(ops, t, p.alpha, p.k);
+                t = sop_apply<EXACT>(ops, t, p.alpha, p.k);
                 float w;
                 if (ops.mop() == FMM_MOP_SEL2ND) {
                     w = y[u][e];
