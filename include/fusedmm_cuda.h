@@ -89,7 +89,14 @@ enum {
     FMM_HOST_PTRS = 0,         /* X, Y, Z are host pointers (default)       */
     FMM_DEVICE_PTRS = 1u << 0, /* X, Y, Z are device pointers on shard 0's
                                   device; single-shard contexts only        */
-    FMM_ASYNC = 1u << 1,       /* with FMM_DEVICE_PTRS: do not synchronize  */
+    FMM_ASYNC = 1u << 1,       /* do not synchronize. Device pointers: the
+                                  kernels are enqueued on the shard stream.
+                                  Host pointers: upload / kernels / download
+                                  are pipelined on three streams over two
+                                  device buffer slots (call k's download
+                                  overlaps call k+1's upload); host buffers
+                                  must stay valid (pinned for overlap) until
+                                  fmm_sync                                  */
     FMM_EXACT = 1u << 2,       /* force bit-exact scheme    */
     FMM_FAST = 1u << 3         /* force reassociating scheme (FMA, splits)  */
 };
@@ -168,6 +175,13 @@ fmm_status fmm_run(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec,
 /* iters fused calls with X <- Z between them (square A, Y = X), the Z slices
  * exchanged between shards on the device. X is the host m x d input and
  * receives the final iterate. */
+/* Wait for every call enqueued with FMM_ASYNC on this context. */
+fmm_status fmm_sync(fmm_ctx* ctx);
+
+/* Page-locked (pinned, portable) host buffers for FMM_ASYNC host calls. */
+fmm_status fmm_host_alloc(void** ptr, size_t bytes);
+fmm_status fmm_host_free(void* ptr);
+
 fmm_status fmm_iterate(fmm_ctx* ctx, const fmm_graph* g,
                        const fmm_opspec* spec, int64_t d, float* X, int iters,
                        uint32_t flags, fmm_stats* stats);

@@ -67,6 +67,9 @@ SIGNATURES = {
                           C.c_uint32, C.POINTER(fmm_stats)]),
     "fmm_iterate": (C.c_int, [_P, _P, C.POINTER(fmm_opspec), C.c_int64, _P, C.c_int,
                               C.c_uint32, C.POINTER(fmm_stats)]),
+    "fmm_sync": (C.c_int, [_P]),
+    "fmm_host_alloc": (C.c_int, [C.POINTER(_P), C.c_size_t]),
+    "fmm_host_free": (C.c_int, [_P]),
 }
 
 _lib = None

@@ -10,11 +10,13 @@
 #include "fmm_kernels.cuh"
 #include "fmm_dispatch.cuh"
 #include "fmm_plan.h"
+#include "fmm_sched.cuh"
 
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <stdexcept>
@@ -30,12 +32,21 @@ struct DevBuf {
 
 struct Shard {
     int dev = 0;
+    int num_sms = 148;
     cudaStream_t own = nullptr;
     cudaStream_t ext = nullptr;
     bool use_ext = false;  // ext may legitimately be the legacy NULL stream
     DevBuf X, Y, Z, Xb, partial;
     cudaEvent_t ev_start = nullptr, ev_k0 = nullptr, ev_k1 = nullptr, ev_end = nullptr,
                 ev_copy = nullptr;
+    // host-pointer FMM_ASYNC pipeline: two buffer slots, copy-in / compute /
+    // copy-out on three streams, so call k's Z download overlaps call k+1's
+    // X upload (PCIe is full duplex) and the kernels
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    DevBuf aX[2], aY[2], aZ[2];
+    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr},
+                ev_out[2] = {nullptr, nullptr};
+    int aslot = 0;
     cudaStream_t stream() const { return use_ext ? ext : own; }
 };
 
@@ -50,8 +61,20 @@ struct fmm_ctx {
 
 namespace {
 
+// Persistent-kernel work lists of one shard for one (gpw, u) shape.
+struct SchedDev {
+    int gpw = 0, u = 0, warps = 0;
+    int32_t* group_item_begin = nullptr;
+    int4* items = nullptr;
+    int32_t* warp_steps = nullptr;
+    int32_t* empty_rows = nullptr;
+    int64_t n_empty = 0;
+};
+
 struct GShard {
     int shard = 0;
+    std::shared_ptr<fmm::ShardPlan> plan;  // host copy, for lazily built schedules
+    std::vector<SchedDev> scheds;
     int64_t row_begin = 0, row_end = 0, nnz = 0;
     int64_t n_split_rows = 0, n_wide_rows = 0, n_chunks = 0, n_slots = 0, nonempty = 0, max_degree = 0;
     int64_t* row_ptr = nullptr;
@@ -175,9 +198,37 @@ bool launch_rows(const fmm::KParams& p, int pattern, int d, bool exact, bool a16
 
 // Launch the fused kernels of one shard: rows (+ chunks) then the combine.
 // Returns the number of kernels launched, or -1 if no instantiation fits.
-int launch_shard(const GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, bool exact,
+// Persistent-kernel work lists for (gpw, u) on this shard, built on first use
+// from the host copy of the plan (synchronous upload, outside timed regions).
+SchedDev* get_sched(GShard& gs, int gpw, int u, int warps) {
+    for (SchedDev& sd : gs.scheds)
+        if (sd.gpw == gpw && sd.u == u && sd.warps == warps) return &sd;
+    if (!gs.plan) return nullptr;
+    const fmm::GroupSchedule S = fmm::build_group_schedule(*gs.plan, warps, gpw, u);
+    SchedDev sd;
+    sd.gpw = gpw;
+    sd.u = u;
+    sd.warps = warps;
+    sd.n_empty = static_cast<int64_t>(S.empty_rows.size());
+    std::vector<int4> items(S.items.size());
+    std::memcpy(items.data(), S.items.data(), items.size() * sizeof(int4));
+    if (upload_vec(nullptr, S.group_item_begin, &sd.group_item_begin) != FMM_OK ||
+        upload_vec(nullptr, items, &sd.items) != FMM_OK ||
+        upload_vec(nullptr, S.warp_steps, &sd.warp_steps) != FMM_OK ||
+        upload_vec(nullptr, S.empty_rows, &sd.empty_rows) != FMM_OK) {
+        for (void* q : {static_cast<void*>(sd.group_item_begin), static_cast<void*>(sd.items),
+                        static_cast<void*>(sd.warp_steps), static_cast<void*>(sd.empty_rows)})
+            if (q) cudaFree(q);
+        cudaGetLastError();
+        return nullptr;
+    }
+    gs.scheds.push_back(sd);
+    return &gs.scheds.back();
+}
+
+int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, bool exact,
                  const float* X, int64_t row0, const float* Y, float* Z, float* partial,
-                 const float* val, int variant, cudaStream_t stream) {
+                 const float* val, int variant, int num_sms, cudaStream_t stream) {
     fmm::KParams p{};
     p.row_ptr = gs.row_ptr;
     p.col = gs.col;
@@ -215,6 +266,51 @@ int launch_shard(const GShard& gs, const fmm_opspec& spec, int pattern, int64_t 
                      (partial == nullptr || aligned(partial, 16)) && (a % 16 == 0);
     const bool a8 = (d % 2 == 0) && aligned(X, 8) && aligned(Y, 8) && aligned(Z, 8) &&
                     (partial == nullptr || aligned(partial, 8));
+    // fast scheme, hot patterns: the persistent cp.async-pipelined kernel
+    int gpw = 0, su = 0;
+    const bool sched_pattern = pattern == FMM_PATTERN_SIGMOID_EMBED || pattern == FMM_PATTERN_TDIST ||
+                               pattern == FMM_PATTERN_FR_LAYOUT;
+    // FMM_VARIANT -4 / -3: persistent pipelined kernel (shape 0 / 1), opt-in:
+    // on config 2 it matches but does not beat the row kernel, both sit near
+    // the L2->SM bandwidth. -1 (default), -2, >= 0: row kernel.
+    const int sv = variant == -3 ? 1 : 0;
+    if (!exact && (variant == -4 || variant == -3) && a16 && sched_pattern && gs.nnz < INT32_MAX &&
+        fmm::sched_shape_for(static_cast<int>(d), sv, &gpw, &su)) {
+        SchedDev* sd = get_sched(gs, gpw, su, num_sms * 8);
+        if (sd) {
+            fmm::SchedParams sp{};
+            sp.col = gs.col;
+            sp.val = val;
+            sp.X = X;
+            sp.Y = Y;
+            sp.Z = Z;
+            sp.partial = partial;
+            sp.group_item_begin = sd->group_item_begin;
+            sp.items = sd->items;
+            sp.warp_steps = sd->warp_steps;
+            sp.empty_rows = sd->empty_rows;
+            sp.n_empty = sd->n_empty;
+            sp.row0 = row0;
+            sp.d = static_cast<int>(d);
+            sp.vop = spec.vop; sp.rop = spec.rop; sp.sop = spec.sop; sp.mop = spec.mop; sp.aop = spec.aop;
+            sp.alpha = spec.alpha;
+            sp.k = spec.k;
+            bool ok = false;
+            if (pattern == FMM_PATTERN_SIGMOID_EMBED) ok = fmm::launch_sched_sigmoid(sp, static_cast<int>(d), sv, num_sms, stream);
+            else if (pattern == FMM_PATTERN_TDIST) ok = fmm::launch_sched_tdist(sp, static_cast<int>(d), sv, num_sms, stream);
+            else ok = fmm::launch_sched_fr(sp, static_cast<int>(d), sv, num_sms, stream);
+            if (ok) {
+                int launches = 1;
+                if (split && gs.n_split_rows > 0) {
+                    fmm::fmm_combine_kernel<<<static_cast<unsigned>(gs.n_split_rows), 256, 0, stream>>>(
+                        gs.split_rows, partial, Z, static_cast<int>(d), spec.aop == FMM_AOP_AMAX ? 1 : 0);
+                    ++launches;
+                }
+                return launches;
+            }
+        }
+    }
+    if (variant < -1) variant = -1;
     if (!launch_rows(p, pattern, static_cast<int>(d), exact, a16, a8, variant, stream)) return -1;
     int launches = 1;
     if (split && gs.n_split_rows > 0) {
@@ -242,9 +338,124 @@ fmm_status check_spec(fmm_ctx* ctx, const fmm_opspec* spec, int64_t d) {
     return FMM_OK;
 }
 
+// fmm_run with host pointers and FMM_ASYNC: enqueue upload / fused kernels /
+// download on the shard's copy-in, compute and copy-out streams using buffer
+// slot (call index % 2), then return. The caller keeps X, Y, Z valid (pinned
+// for true overlap) until fmm_sync.
+fmm_status run_host_async(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec& spec, int pattern,
+                          bool exact, int64_t d, const float* X, int64_t ny, const float* Y, float* Z,
+                          fmm_stats* stats) {
+    const size_t row_bytes = static_cast<size_t>(d) * sizeof(float);
+    const bool alias = (X == Y) && (ny == g->m);
+    int launches = 0;
+    size_t aux = 0;
+    fmm_status st;
+    for (size_t s = 0; s < g->shards.size(); ++s) {
+        const GShard& gs = g->shards[s];
+        Shard& sh = ctx->shards[gs.shard];
+        FMM_CK(ctx, cudaSetDevice(sh.dev));
+        if (!sh.s_in) {
+            FMM_CK(ctx, cudaStreamCreateWithFlags(&sh.s_in, cudaStreamNonBlocking));
+            FMM_CK(ctx, cudaStreamCreateWithFlags(&sh.s_out, cudaStreamNonBlocking));
+            for (int i = 0; i < 2; ++i) {
+                FMM_CK(ctx, cudaEventCreateWithFlags(&sh.ev_in[i], cudaEventDisableTiming));
+                FMM_CK(ctx, cudaEventCreateWithFlags(&sh.ev_comp[i], cudaEventDisableTiming));
+                FMM_CK(ctx, cudaEventCreateWithFlags(&sh.ev_out[i], cudaEventDisableTiming));
+                // recorded once so the first waits on them are satisfied
+                FMM_CK(ctx, cudaEventRecord(sh.ev_comp[i], sh.s_in));
+                FMM_CK(ctx, cudaEventRecord(sh.ev_out[i], sh.s_out));
+            }
+        }
+        const int k = sh.aslot;
+        sh.aslot ^= 1;
+        const int64_t srows = gs.row_end - gs.row_begin;
+        // buffers of slot k (a reallocation waits for every stream)
+        const size_t ybytes = std::max<size_t>(1, ny * row_bytes);
+        const size_t xbytes = std::max<size_t>(1, srows * row_bytes);
+        if (sh.aY[k].cap < ybytes || (!alias && sh.aX[k].cap < xbytes) || sh.aZ[k].cap < xbytes) {
+            for (cudaStream_t q : {sh.s_in, sh.s_out, sh.stream()}) FMM_CK(ctx, cudaStreamSynchronize(q));
+        }
+        if ((st = ensure(ctx, sh, sh.aY[k], ybytes)) != FMM_OK) return st;
+        if (!alias && (st = ensure(ctx, sh, sh.aX[k], xbytes)) != FMM_OK) return st;
+        if ((st = ensure(ctx, sh, sh.aZ[k], xbytes)) != FMM_OK) return st;
+        float* part = nullptr;
+        if (!exact && gs.n_slots > 0) {
+            const size_t pb = static_cast<size_t>(gs.n_slots) * row_bytes;
+            if (sh.partial.cap < pb) FMM_CK(ctx, cudaStreamSynchronize(sh.stream()));
+            if ((st = ensure(ctx, sh, sh.partial, pb)) != FMM_OK) return st;
+            part = static_cast<float*>(sh.partial.ptr);
+            aux = std::max(aux, pb);
+        }
+        // upload into slot k once the kernels of call k-2 stopped reading it
+        FMM_CK(ctx, cudaStreamWaitEvent(sh.s_in, sh.ev_comp[k], 0));
+        if (ny > 0) FMM_CK(ctx, cudaMemcpyAsync(sh.aY[k].ptr, Y, ny * row_bytes, cudaMemcpyHostToDevice, sh.s_in));
+        if (!alias && srows > 0)
+            FMM_CK(ctx, cudaMemcpyAsync(sh.aX[k].ptr, X + gs.row_begin * d, srows * row_bytes,
+                                        cudaMemcpyHostToDevice, sh.s_in));
+        FMM_CK(ctx, cudaEventRecord(sh.ev_in[k], sh.s_in));
+        // compute once uploaded and once call k-2's download released Z slot k
+        cudaStream_t cs = sh.stream();
+        FMM_CK(ctx, cudaStreamWaitEvent(cs, sh.ev_in[k], 0));
+        FMM_CK(ctx, cudaStreamWaitEvent(cs, sh.ev_out[k], 0));
+        const float* yd = static_cast<const float*>(sh.aY[k].ptr);
+        const float* xd = alias ? yd : static_cast<const float*>(sh.aX[k].ptr);
+        const int64_t row0 = alias ? gs.row_begin : 0;
+        float* zd = static_cast<float*>(sh.aZ[k].ptr);
+        const int l = launch_shard(const_cast<GShard&>(gs), spec, pattern, d, exact, xd, row0, yd, zd, part,
+                                   gs.val, ctx->variant, sh.num_sms, cs);
+        if (l < 0) return set_err(ctx, FMM_E_UNSUPPORTED, "fused_mm: no kernel for this d / alignment");
+        launches += l;
+        FMM_CK(ctx, cudaGetLastError());
+        FMM_CK(ctx, cudaEventRecord(sh.ev_comp[k], cs));
+        // download after the kernels
+        FMM_CK(ctx, cudaStreamWaitEvent(sh.s_out, sh.ev_comp[k], 0));
+        if (srows > 0)
+            FMM_CK(ctx, cudaMemcpyAsync(Z + (gs.row_begin - g->row_begin) * d, zd, srows * row_bytes,
+                                        cudaMemcpyDeviceToHost, sh.s_out));
+        FMM_CK(ctx, cudaEventRecord(sh.ev_out[k], sh.s_out));
+    }
+    if (stats) {
+        *stats = fmm_stats{};
+        stats->aux_bytes = aux;
+        stats->threads = static_cast<int32_t>(g->shards.size());
+        stats->pattern = pattern;
+        stats->exact = exact ? 1 : 0;
+        stats->launches = launches;
+    }
+    return FMM_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+fmm_status fmm_host_alloc(void** ptr, size_t bytes) {
+    if (!ptr) return FMM_E_INVAL;
+    *ptr = nullptr;
+    const cudaError_t e = cudaHostAlloc(ptr, std::max<size_t>(bytes, 1), cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return e == cudaErrorMemoryAllocation ? FMM_E_OOM : FMM_E_CUDA;
+    }
+    return FMM_OK;
+}
+
+fmm_status fmm_host_free(void* ptr) {
+    if (!ptr) return FMM_OK;
+    return cudaFreeHost(ptr) == cudaSuccess ? FMM_OK : FMM_E_CUDA;
+}
+
+fmm_status fmm_sync(fmm_ctx* ctx) {
+    if (!ctx) return FMM_E_INVAL;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    for (Shard& sh : ctx->shards) {
+        FMM_CK(ctx, cudaSetDevice(sh.dev));
+        if (sh.s_in) FMM_CK(ctx, cudaStreamSynchronize(sh.s_in));
+        FMM_CK(ctx, cudaStreamSynchronize(sh.stream()));
+        if (sh.s_out) FMM_CK(ctx, cudaStreamSynchronize(sh.s_out));
+    }
+    return FMM_OK;
+}
 
 const char* fmm_version(void) { return "libfusedmm_cuda 0.1 (sm_100a)"; }
 
@@ -285,6 +496,7 @@ fmm_status fmm_create(int ngpu, const int* devs, fmm_ctx** out) {
         }
         Shard& sh = ctx->shards[i];
         sh.dev = dev;
+        cudaDeviceGetAttribute(&sh.num_sms, cudaDevAttrMultiProcessorCount, dev);
         if (cudaSetDevice(dev) != cudaSuccess ||
             cudaStreamCreateWithFlags(&sh.own, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreate(&sh.ev_start) != cudaSuccess || cudaEventCreate(&sh.ev_k0) != cudaSuccess ||
@@ -316,11 +528,16 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
     for (Shard& sh : ctx->shards) {
         cudaSetDevice(sh.dev);
         if (sh.own) cudaStreamSynchronize(sh.own);
-        for (DevBuf* b : {&sh.X, &sh.Y, &sh.Z, &sh.Xb, &sh.partial})
+        for (cudaStream_t st : {sh.s_in, sh.s_out})
+            if (st) cudaStreamSynchronize(st);
+        for (DevBuf* b : {&sh.X, &sh.Y, &sh.Z, &sh.Xb, &sh.partial, &sh.aX[0], &sh.aX[1], &sh.aY[0],
+                          &sh.aY[1], &sh.aZ[0], &sh.aZ[1]})
             if (b->ptr) cudaFree(b->ptr);
-        for (cudaEvent_t e : {sh.ev_start, sh.ev_k0, sh.ev_k1, sh.ev_end, sh.ev_copy})
+        for (cudaEvent_t e : {sh.ev_start, sh.ev_k0, sh.ev_k1, sh.ev_end, sh.ev_copy, sh.ev_in[0], sh.ev_in[1],
+                              sh.ev_comp[0], sh.ev_comp[1], sh.ev_out[0], sh.ev_out[1]})
             if (e) cudaEventDestroy(e);
-        if (sh.own) cudaStreamDestroy(sh.own);
+        for (cudaStream_t st : {sh.own, sh.s_in, sh.s_out})
+            if (st) cudaStreamDestroy(st);
     }
     delete ctx;
     return FMM_OK;
@@ -410,6 +627,7 @@ fmm_status fmm_graph_upload(fmm_ctx* ctx, int64_t m, int64_t n, const int64_t* r
             break;
         }
         gs.nnz = P.nnz;
+        gs.plan = std::make_shared<fmm::ShardPlan>(P);
         gs.n_split_rows = P.n_split_rows;
         gs.n_wide_rows = P.n_wide_rows;
         gs.n_chunks = static_cast<int64_t>(P.chunks.size());
@@ -472,6 +690,10 @@ fmm_status fmm_graph_free(fmm_graph* g) {
     if (!g) return FMM_E_INVAL;
     for (GShard& gs : g->shards) {
         cudaSetDevice(g->ctx->shards[gs.shard].dev);
+        for (SchedDev& sd : gs.scheds)
+            for (void* q : {static_cast<void*>(sd.group_item_begin), static_cast<void*>(sd.items),
+                            static_cast<void*>(sd.warp_steps), static_cast<void*>(sd.empty_rows)})
+                if (q) cudaFree(q);
         for (void* p : {static_cast<void*>(gs.row_ptr), static_cast<void*>(gs.col), static_cast<void*>(gs.val),
                         static_cast<void*>(gs.order), static_cast<void*>(gs.chunks),
                         static_cast<void*>(gs.split_rows)})
@@ -529,6 +751,8 @@ fmm_status fmm_run(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec, int
     bool exact = default_exact(pattern, d);
     if (flags & FMM_EXACT) exact = true;
     if (flags & FMM_FAST) exact = false;
+    if (!dev_ptrs && (flags & FMM_ASYNC))
+        return run_host_async(ctx, g, *spec, pattern, exact, d, X, ny, Y, Z, stats);
     const size_t row_bytes = static_cast<size_t>(d) * sizeof(float);
     const bool alias = (X == Y) && (ny == g->m);
     int launches = 0;
@@ -578,7 +802,8 @@ fmm_status fmm_run(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec, int
             aux = std::max(aux, pb);
         }
         if (timed) FMM_CK(ctx, cudaEventRecord(sh.ev_k0, stream));
-        const int l = launch_shard(gs, *spec, pattern, d, exact, xd, row0, yd, zd, part, gs.val, ctx->variant, stream);
+        const int l = launch_shard(const_cast<GShard&>(gs), *spec, pattern, d, exact, xd, row0, yd, zd, part,
+                                   gs.val, ctx->variant, sh.num_sms, stream);
         if (l < 0) return set_err(ctx, FMM_E_UNSUPPORTED, "fused_mm: no kernel for this d / alignment");
         launches += l;
         FMM_CK(ctx, cudaGetLastError());
@@ -664,9 +889,9 @@ fmm_status fmm_iterate(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec,
                     if (q != s) FMM_CK(ctx, cudaStreamWaitEvent(sh.stream(), ctx->shards[g->shards[q].shard].ev_copy, 0));
             float* xc = static_cast<float*>(cur == 0 ? sh.Y.ptr : sh.Xb.ptr);
             float* xn = static_cast<float*>(cur == 0 ? sh.Xb.ptr : sh.Y.ptr);
-            const int l = launch_shard(gs, *spec, pattern, d, exact, xc, gs.row_begin, xc,
+            const int l = launch_shard(const_cast<GShard&>(gs), *spec, pattern, d, exact, xc, gs.row_begin, xc,
                                        xn + gs.row_begin * d, static_cast<float*>(sh.partial.ptr),
-                                       gs.val, ctx->variant, sh.stream());
+                                       gs.val, ctx->variant, sh.num_sms, sh.stream());
             if (l < 0) return set_err(ctx, FMM_E_UNSUPPORTED, "iterate: no kernel for this d / alignment");
             launches += l;
             FMM_CK(ctx, cudaGetLastError());

@@ -237,6 +237,73 @@ __device__ __forceinline__ void consume_edges(const Ops& ops, const KParams& p, 
     // ASUM accumulations may run predicated (an invalid edge adds +0);
     // AMAX and the exact scheme skip invalid edges explicitly.
     const bool predicated = !EXACT && ops.aop() == FMM_AOP_ASUM;
+    if constexpr (VEC % 2 == 0 && !MASKED) {
+        // Packed f32x2 path (Blackwell FFMA2/FADD2/FMUL2: two lanes of math per
+        // instruction), fast scheme only: scalar messages with ASUM. (The
+        // exact scheme stays scalar: ptxas may contract packed mul+add.)
+        if (!EXACT && ops.aop() == FMM_AOP_ASUM && ops.rop() != FMM_ROP_NOOP &&
+            ops.rop() != FMM_ROP_RMUL && ops.mop() != FMM_MOP_SEL2ND) {
+            float s[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int e = 0; e < NE; e += 2) {
+                    const float2 xv = make_float2(x[e], x[e + 1]);
+                    const float2 yv = make_float2(y[u][e], y[u][e + 1]);
+                    float2& acc = ((e >> 1) & 1) ? acc1 : acc0;
+                    if (ops.vop() == FMM_VOP_MUL && ops.rop() == FMM_ROP_RSUM) {
+                        acc = __ffma2_rn(xv, yv, acc);
+                    } else {
+                        float2 t;
+                        switch (ops.vop()) {
+                            case FMM_VOP_ADD: t = __fadd2_rn(xv, yv); break;
+                            case FMM_VOP_MUL: t = __fmul2_rn(xv, yv); break;
+                            case FMM_VOP_SEL2ND: t = yv; break;
+                            default: t = __ffma2_rn(yv, make_float2(-1.f, -1.f), xv); break;  // x - y
+                        }
+                        if (ops.rop() == FMM_ROP_RSUM) acc = __fadd2_rn(acc, t);
+                        else acc = __ffma2_rn(t, t, acc);  // NORM / SQNORM
+                    }
+                }
+                s[u] = (acc0.x + acc0.y) + (acc1.x + acc1.y);
+            }
+            if (LPG > 1) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) s[u] = group_sum<LPG>(s[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                float sv = s[u];
+                if (ops.rop() == FMM_ROP_NORM) sv = sqrtf(sv);
+                float h = sop_apply<EXACT>(ops, sv, p.alpha, p.k);
+                h = ok[u] ? h : 0.0f;
+                if (ops.mop() == FMM_MOP_MUL_VOP) h *= a[u];
+                const float2 h2 = make_float2(h, h);
+#pragma unroll
+                for (int e = 0; e < NE; e += 2) {
+                    const float2 yv = make_float2(y[u][e], y[u][e + 1]);
+                    float2 zv = make_float2(z[e], z[e + 1]);
+                    if (ops.mop() == FMM_MOP_MUL_VOP) {
+                        const float2 xv = make_float2(x[e], x[e + 1]);
+                        float2 t;
+                        switch (ops.vop()) {
+                            case FMM_VOP_ADD: t = __fadd2_rn(xv, yv); break;
+                            case FMM_VOP_MUL: t = __fmul2_rn(xv, yv); break;
+                            case FMM_VOP_SEL2ND: t = yv; break;
+                            default: t = __ffma2_rn(yv, make_float2(-1.f, -1.f), xv); break;
+                        }
+                        zv = __ffma2_rn(h2, t, zv);
+                    } else {
+                        zv = __ffma2_rn(h2, yv, zv);
+                    }
+                    z[e] = zv.x;
+                    z[e + 1] = zv.y;
+                }
+            }
+            return;
+        }
+    }
     if (ops.rop() != FMM_ROP_NOOP) {
         const bool prod = rop_is_product(ops.rop());
         float s[U];

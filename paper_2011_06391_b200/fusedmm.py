@@ -373,6 +373,10 @@ class Context:
             _raise(st, None, "fmm_create failed (no CUDA device?)")
         self.h = h
 
+    def sync(self) -> None:
+        """Wait for every FMM_ASYNC call enqueued on this context."""
+        _raise(_lib.lib().fmm_sync(self.h), self.h)
+
     def set_stream(self, shard: int, stream_handle: int) -> None:
         _raise(_lib.lib().fmm_set_stream(self.h, shard, C.c_void_p(stream_handle)), self.h)
 
@@ -389,6 +393,31 @@ class Context:
 
 
 _contexts: dict = {}
+
+
+class PinnedBuffer:
+    """Page-locked host memory from libfusedmm_cuda (fmm_host_alloc), viewed as
+    a numpy array; the host side of FMM_ASYNC pipelined calls."""
+
+    def __init__(self, shape, dtype=np.float32):
+        self.nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        p = C.c_void_p()
+        _raise(_lib.lib().fmm_host_alloc(C.byref(p), self.nbytes))
+        self.ptr = p
+        buf = (C.c_byte * max(self.nbytes, 1)).from_address(p.value)
+        self.array = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+
+    def close(self) -> None:
+        if getattr(self, "ptr", None):
+            self.array = None
+            _lib.lib().fmm_host_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def device_count() -> int:
