@@ -98,7 +98,10 @@ enum {
                                   must stay valid (pinned for overlap) until
                                   fmm_sync                                  */
     FMM_EXACT = 1u << 2,       /* force bit-exact scheme    */
-    FMM_FAST = 1u << 3         /* force reassociating scheme (FMA, splits)  */
+    FMM_FAST = 1u << 3,        /* force reassociating scheme (FMA, splits)  */
+    FMM_EXCHANGE_COPIES = 1u << 4 /* fmm_iterate: exchange Z slices with
+                                  peer copies after the kernels instead of
+                                  the fused P2P-store epilogue (default)    */
 };
 
 /* Mirrors KernelStats (kernel.hpp:51-55) plus device-side evidence. */

@@ -22,6 +22,7 @@ FMM_DEVICE_PTRS = 1 << 0
 FMM_ASYNC = 1 << 1
 FMM_EXACT = 1 << 2
 FMM_FAST = 1 << 3
+FMM_EXCHANGE_COPIES = 1 << 4
 
 
 class fmm_opspec(C.Structure):

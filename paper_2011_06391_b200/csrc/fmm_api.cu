@@ -55,6 +55,7 @@ struct Shard {
 struct fmm_ctx {
     std::vector<Shard> shards;
     int variant = -1;  // kernel shape variant (FMM_VARIANT env, tuning only)
+    bool p2p_ok = true;  // every pair of distinct shard devices has peer access
     std::string err;
     std::mutex mu;
 };
@@ -228,8 +229,15 @@ SchedDev* get_sched(GShard& gs, int gpw, int u, int warps) {
 
 int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, bool exact,
                  const float* X, int64_t row0, const float* Y, float* Z, float* partial,
-                 const float* val, int variant, int num_sms, cudaStream_t stream) {
+                 const float* val, int variant, int num_sms, cudaStream_t stream,
+                 const fmm::PeerOut* peers = nullptr) {
     fmm::KParams p{};
+    fmm::PeerOut po{};
+    if (peers) {
+        po = *peers;
+        for (int q = 0; q < po.n; ++q) p.zpeer[q] = po.p[q];
+        p.n_peer = po.n;
+    }
     p.row_ptr = gs.row_ptr;
     p.col = gs.col;
     p.val = val;
@@ -274,7 +282,7 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
     // on config 2 it matches but does not beat the row kernel, both sit near
     // the L2->SM bandwidth. -1 (default), -2, >= 0: row kernel.
     const int sv = variant == -3 ? 1 : 0;
-    if (!exact && (variant == -4 || variant == -3) && a16 && sched_pattern && gs.nnz < INT32_MAX &&
+    if (!exact && (variant == -4 || variant == -3) && a16 && sched_pattern && gs.nnz < INT32_MAX && po.n == 0 &&
         fmm::sched_shape_for(static_cast<int>(d), sv, &gpw, &su)) {
         SchedDev* sd = get_sched(gs, gpw, su, num_sms * 8);
         if (sd) {
@@ -303,7 +311,7 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
                 int launches = 1;
                 if (split && gs.n_split_rows > 0) {
                     fmm::fmm_combine_kernel<<<static_cast<unsigned>(gs.n_split_rows), 256, 0, stream>>>(
-                        gs.split_rows, partial, Z, static_cast<int>(d), spec.aop == FMM_AOP_AMAX ? 1 : 0);
+                        gs.split_rows, partial, Z, static_cast<int>(d), spec.aop == FMM_AOP_AMAX ? 1 : 0, po);
                     ++launches;
                 }
                 return launches;
@@ -315,7 +323,7 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
     int launches = 1;
     if (split && gs.n_split_rows > 0) {
         fmm::fmm_combine_kernel<<<static_cast<unsigned>(gs.n_split_rows), 256, 0, stream>>>(
-            gs.split_rows, partial, Z, static_cast<int>(d), spec.aop == FMM_AOP_AMAX ? 1 : 0);
+            gs.split_rows, partial, Z, static_cast<int>(d), spec.aop == FMM_AOP_AMAX ? 1 : 0, po);
         ++launches;
     }
     return launches;
@@ -517,6 +525,9 @@ fmm_status fmm_create(int ngpu, const int* devs, fmm_ctx** out) {
                 cudaSetDevice(a);
                 const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
                 if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else if (e != cudaSuccess) ctx->p2p_ok = false;
+            } else {
+                ctx->p2p_ok = false;  // kernels cannot store into that peer
             }
         }
     *out = ctx;
@@ -878,8 +889,15 @@ fmm_status fmm_iterate(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec,
         if (m > 0) FMM_CK(ctx, cudaMemcpyAsync(sh.Y.ptr, X, m * row_bytes, cudaMemcpyHostToDevice, sh.stream()));
         FMM_CK(ctx, cudaEventRecord(sh.ev_k0, sh.stream()));
     }
+    // Fused exchange (default): each shard's kernels store every finished z
+    // row into its own next buffer AND into every peer's (P2P over NVLink, or
+    // plain stores for shards sharing a device), so the all-gather overlaps
+    // the compute; kernel completion (events) orders the next iteration.
+    // FMM_EXCHANGE_COPIES: post-kernel cudaMemcpyPeerAsync slices instead.
+    const bool fused = S > 1 && S - 1 <= fmm::kMaxPeers && ctx->p2p_ok && !(flags & FMM_EXCHANGE_COPIES);
     int cur = 0;  // 0: Y holds the iterate, 1: Xb holds it
     for (int it = 0; it < iters; ++it) {
+        const bool exchange = it + 1 < iters && S > 1;
         for (int s = 0; s < S; ++s) {
             const GShard& gs = g->shards[s];
             Shard& sh = ctx->shards[gs.shard];
@@ -889,14 +907,22 @@ fmm_status fmm_iterate(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec,
                     if (q != s) FMM_CK(ctx, cudaStreamWaitEvent(sh.stream(), ctx->shards[g->shards[q].shard].ev_copy, 0));
             float* xc = static_cast<float*>(cur == 0 ? sh.Y.ptr : sh.Xb.ptr);
             float* xn = static_cast<float*>(cur == 0 ? sh.Xb.ptr : sh.Y.ptr);
+            fmm::PeerOut po{};
+            if (fused && exchange)
+                for (int q = 0; q < S; ++q) {
+                    if (q == s) continue;
+                    Shard& sq = ctx->shards[g->shards[q].shard];
+                    po.p[po.n++] = static_cast<float*>(cur == 0 ? sq.Xb.ptr : sq.Y.ptr) + gs.row_begin * d;
+                }
             const int l = launch_shard(const_cast<GShard&>(gs), *spec, pattern, d, exact, xc, gs.row_begin, xc,
                                        xn + gs.row_begin * d, static_cast<float*>(sh.partial.ptr),
-                                       gs.val, ctx->variant, sh.num_sms, sh.stream());
+                                       gs.val, ctx->variant, sh.num_sms, sh.stream(), &po);
             if (l < 0) return set_err(ctx, FMM_E_UNSUPPORTED, "iterate: no kernel for this d / alignment");
             launches += l;
             FMM_CK(ctx, cudaGetLastError());
+            if (fused && exchange) FMM_CK(ctx, cudaEventRecord(sh.ev_copy, sh.stream()));
         }
-        if (it + 1 < iters && S > 1) {
+        if (exchange && !fused) {
             // exchange: every shard pushes its fresh Z slice into every peer's next buffer
             for (int s = 0; s < S; ++s) {
                 const GShard& gs = g->shards[s];

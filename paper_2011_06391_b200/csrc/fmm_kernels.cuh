@@ -31,6 +31,13 @@
 
 namespace fmm {
 
+constexpr int kMaxPeers = 7;  // 8 GPUs per NVSwitch domain in one process
+
+struct PeerOut {
+    float* p[kMaxPeers];
+    int n;
+};
+
 struct KParams {
     const int64_t* row_ptr;  // shard-local, rebased to 0, rows+1 entries
     const int32_t* col;      // shard-local edge columns (narrowed to int32)
@@ -50,6 +57,11 @@ struct KParams {
     // dynamic op codes (used by DOps only)
     int vop, rop, sop, mop, aop;
     float alpha, k;
+    // fused exchange: every final z row is also stored to zpeer[q] + r*d —
+    // the other shards' next-iterate buffers, reached over NVLink (P2P) — so
+    // the per-iteration all-gather rides on the kernel's own stores
+    float* zpeer[kMaxPeers];
+    int n_peer;
 };
 
 // ---------------------------------------------------------------- op kinds
@@ -525,10 +537,17 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
                 }
             }
         }
-        // group gg stores vectors i with i % GPW == gg
+        // group gg stores vectors i with i % GPW == gg; final rows (not chunk
+        // partials) also go straight into the peers' next-iterate buffers
+        const bool to_peers = warp >= p.n_chunk_items;
 #pragma unroll
         for (int i = 0; i < NV; ++i)
-            if ((i % GPW) == g && elem_ok[i]) store_vec<VEC>(out + (i * LPG + gl) * VEC, &z[i * VEC]);
+            if ((i % GPW) == g && elem_ok[i]) {
+                store_vec<VEC>(out + (i * LPG + gl) * VEC, &z[i * VEC]);
+                if (to_peers)
+                    for (int q = 0; q < p.n_peer; ++q)
+                        store_vec<VEC>(p.zpeer[q] + r * d + (i * LPG + gl) * VEC, &z[i * VEC]);
+            }
         return;
     }
 
@@ -573,7 +592,11 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
         if (active) {
 #pragma unroll
             for (int i = 0; i < NV; ++i)
-                if (elem_ok[i]) store_vec<VEC>(out + (i * LPG + gl) * VEC, &z[i * VEC]);
+                if (elem_ok[i]) {
+                    store_vec<VEC>(out + (i * LPG + gl) * VEC, &z[i * VEC]);
+                    for (int q = 0; q < p.n_peer; ++q)
+                        store_vec<VEC>(p.zpeer[q] + r * d + (i * LPG + gl) * VEC, &z[i * VEC]);
+                }
         }
     }
 }
@@ -584,7 +607,7 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
 // a contiguous chunk range, then lane 0 folds the Q results in order.
 __global__ void __launch_bounds__(256)
 fmm_combine_kernel(const int4* __restrict__ split, const float* __restrict__ partial,
-                   float* __restrict__ Z, int d, int is_max) {
+                   float* __restrict__ Z, int d, int is_max, const PeerOut peers) {
     __shared__ float red[256];
     const int4 s = split[blockIdx.x];
     const int K = s.z;
@@ -612,6 +635,7 @@ fmm_combine_kernel(const int4* __restrict__ split, const float* __restrict__ par
                 acc = is_max ? (acc < v ? v : acc) : __fadd_rn(acc, v);
             }
             zr[j] = acc;
+            for (int q = 0; q < peers.n; ++q) peers.p[q][static_cast<int64_t>(s.x) * d + j] = acc;
         }
         return;
     }
@@ -649,6 +673,7 @@ fmm_combine_kernel(const int4* __restrict__ split, const float* __restrict__ par
             acc = is_max ? (acc < v ? v : acc) : __fadd_rn(acc, v);
         }
         zr[j] = acc;
+        for (int qq = 0; qq < peers.n; ++qq) peers.p[qq][static_cast<int64_t>(s.x) * d + j] = acc;
     }
 }
 

@@ -96,3 +96,20 @@ def test_async_host_pipeline_matches_sync_calls():
     for x, z in zip(Xs, Zs):
         ref = F.fused_mm(w.A, F.DenseMatrix.wrap(x), F.DenseMatrix.wrap(x), w.spec, 1)
         check_exact(z, ref.array)
+
+
+@pytest.mark.parametrize("cfg", [3, 5, 2])
+def test_fused_exchange_iterate(cfg):
+    """fmm_iterate on 3 shards: the default fused exchange (each kernel
+    stores its finished rows into every peer's next-iterate buffer) and the
+    post-kernel peer-copy exchange both reproduce the single-shard iterate
+    bitwise."""
+    from paper_2011_06391_b200 import _lib
+    w = configs.get(cfg, small=True)
+    iters = max(w.iters, 2)
+    ref = F.iterate(w.A, w.X, w.spec, iters, 1)
+    g = F.DeviceGraph(F.Context([0, 0, 0]), w.A)
+    for flags in (0, _lib.FMM_EXCHANGE_COPIES):
+        X = w.X.array.copy()
+        g.iterate_host(X, w.d, w.spec, iters, flags)
+        check_exact(X, ref.array)
