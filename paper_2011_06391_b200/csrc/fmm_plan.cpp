@@ -40,11 +40,15 @@ std::string validate_row_ptr(int64_t m, const int64_t* row_ptr) {
 
 namespace {
 // Degree bucket: 0 for empty rows, else 1 + 4*floor(log2 deg) + next two bits.
+// Degree buckets, monotone in deg: power-of-two below 8, so narrow-degree
+// graphs (lattices) keep their natural row order — sequential x_u / Z / CSR
+// traffic — and quarter-octaves from 8 up, so rows sharing a warp have
+// similar lengths and power-law hubs run first (LPT).
 inline int degree_bucket(int64_t deg) {
     if (deg <= 0) return 0;
     const int lg = 63 - __builtin_clzll(static_cast<unsigned long long>(deg));
-    const int frac = lg >= 2 ? static_cast<int>((deg >> (lg - 2)) & 3) : static_cast<int>((deg << (2 - lg)) & 3);
-    return 1 + 4 * lg + frac;
+    if (lg < 3) return 1 + lg;
+    return 4 + 4 * (lg - 3) + static_cast<int>((deg >> (lg - 2)) & 3);
 }
 }  // namespace
 

@@ -39,7 +39,7 @@ struct ShardPlan {
     int64_t edge_begin = 0, nnz = 0;      // absolute edge offset, count
     std::vector<int64_t> local_row_ptr;   // rebased, rows+1
     // Rows ordered heavy-first: rows with degree > kChunkEdges first, then by
-    // descending log2-quarter degree bucket, stable (natural order) inside a
+    // descending power-of-two degree bucket, stable (natural order) inside a
     // bucket so light rows keep their memory locality.
     std::vector<int32_t> order;
     int64_t n_split_rows = 0;             // prefix of `order` cut into chunks
