@@ -89,7 +89,8 @@ def build_gen(force: bool = False) -> Path:
     out = LIB / "libfmm_gen.so"
     src = CSRC / "fmm_gen.cpp"
     if force or _stale(out, [src], 0.0):
-        _run(["g++", "-O3", "-std=c++17", "-fPIC", "-march=x86-64-v3", "-shared", "-o", str(out), str(src)])
+        _run(["g++", "-O3", "-std=c++17", "-fPIC", "-march=x86-64-v3", "-pthread", "-shared", "-o", str(out),
+              str(src)])
     return out
 
 

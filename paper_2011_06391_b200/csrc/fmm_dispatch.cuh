@@ -39,6 +39,8 @@ inline bool launch_aligned(const KParams& p, const Ops& ops, int d, int variant,
                 if (variant == 0) { launch_one<Ops, 8, 4, 1, 8, EXACT, false>(p, ops, s); return true; }
                 if (variant == 2) { launch_one<Ops, 2, 4, 4, 4, EXACT, false>(p, ops, s); return true; }
                 if (variant == 3) { launch_one<Ops, 8, 4, 1, 16, EXACT, false>(p, ops, s); return true; }
+                if (variant == 4) { launch_one<Ops, 4, 4, 2, 8, EXACT, false>(p, ops, s); return true; }
+                if (variant == 5) { launch_one<Ops, 2, 4, 4, 2, EXACT, false>(p, ops, s); return true; }
             }
             launch_one<Ops, 4, 4, 2, 4, EXACT, false>(p, ops, s); return true;
         case 64:
