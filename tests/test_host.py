@@ -122,3 +122,15 @@ def test_full_size_graphs_match_survey_probe():
     w4 = configs.config4()
     assert w4.A.nnz() == 25_157_628 and int(np.diff(w4.A.row_ptr).max()) == 15
     assert w4.alg_bytes() == 402_554_840
+
+
+def test_bulk_mt19937_64_matches_std():
+    # the vectorised generator behind the parallel R-MAT stream is
+    # bit-identical to std::mt19937_64 across uneven block boundaries
+    import ctypes as C
+    from paper_2011_06391_b200 import _lib
+    G = _lib.gen()
+    G.fmmgen_mt64_check.restype = C.c_int64
+    G.fmmgen_mt64_check.argtypes = [C.c_uint64, C.c_int64]
+    for seed in (0, 1, 4, 5489, 2**63 + 7):
+        assert G.fmmgen_mt64_check(seed, 300_000) == 0
