@@ -36,6 +36,21 @@ PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM_GBS = 6650.0
 
 
+def ncu_traffic(cfg: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the row
+    kernel for this config, from the newest committed `ncu --set full`
+    capture (profiles/<tag>_summary.json), or (None, why)."""
+    for path in sorted((ROOT / "profiles").glob("r*_summary.json"), reverse=True):
+        try:
+            s = json.loads(path.read_text())
+        except Exception:
+            continue
+        for name, rep in s.get("reports", {}).items():
+            if name.endswith(f"config{cfg}_rows") and "dram_bytes_total" in rep:
+                return rep["dram_bytes_total"], f"{path.name}:{name} (ncu --set full, one launch)"
+    return None, "no committed ncu capture for this config"
+
+
 def hbm_peak():
     try:
         p = json.loads(PEAKS_FILE.read_text())
@@ -309,7 +324,8 @@ def run_ours(args):
                        "split_rows": int(info.split_rows), "max_degree": int(info.max_degree),
                        "gen_seconds": round(gen_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": ncu_traffic(args.config)[0],
+                         "traffic_source": ncu_traffic(args.config)[1],
                          "alg_bytes_per_launch": alg, "peak_source": peak_src,
                          "kernel": "fmm_rows_kernel (+fmm_combine_kernel)"},
             "e2e": {"value": e2e_value, "unit": "nnz*d/s", "h2d_bytes_per_step": int(m * d * 4),
