@@ -203,9 +203,15 @@ def run_ours(args):
     from paper_2011_06391_b200 import _lib
 
     rank, world, local = dist_env()
+    # FMM_BENCH_SHARE_GPU=1 (testing only): every rank on GPU 0 with gloo, to
+    # exercise the multi-rank code path on a one-GPU box (timings meaningless)
+    share = os.environ.get("FMM_BENCH_SHARE_GPU") == "1"
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(0 if share else local)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
