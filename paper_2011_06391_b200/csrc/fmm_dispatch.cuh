@@ -7,7 +7,7 @@
 
 namespace fmm {
 
-template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED>
+template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED, int MINB = 0>
 inline void launch_one(const KParams& p, const Ops& ops, cudaStream_t stream) {
     constexpr int kThreads = 256;
     constexpr int GPW = 32 / LPG;
@@ -15,7 +15,7 @@ inline void launch_one(const KParams& p, const Ops& ops, cudaStream_t stream) {
     const int64_t warps = wide + (p.n_narrow_rows + GPW - 1) / GPW;
     if (warps <= 0) return;
     const int64_t blocks = (warps + (kThreads / 32) - 1) / (kThreads / 32);
-    fmm_rows_kernel<Ops, LPG, VEC, NV, UNROLL, EXACT, MASKED>
+    fmm_rows_kernel<Ops, LPG, VEC, NV, UNROLL, EXACT, MASKED, MINB>
         <<<static_cast<unsigned>(blocks), kThreads, 0, stream>>>(p, ops);
 }
 
@@ -26,11 +26,11 @@ inline bool launch_aligned(const KParams& p, const Ops& ops, int d, int variant,
     switch (d) {
         case 1: launch_one<Ops, 1, 1, 1, 8, EXACT, false>(p, ops, s); return true;
         case 2:
-            if constexpr (!EXACT) {
-                if (variant == 1) { launch_one<Ops, 1, 2, 1, 4, EXACT, false>(p, ops, s); return true; }
-                if (variant == 2) { launch_one<Ops, 1, 2, 1, 16, EXACT, false>(p, ops, s); return true; }
-            }
-            launch_one<Ops, 1, 2, 1, 8, EXACT, false>(p, ops, s); return true;
+            if (variant == 1) { launch_one<Ops, 1, 2, 1, 4, EXACT, false>(p, ops, s); return true; }
+            if (variant == 2) { launch_one<Ops, 1, 2, 1, 16, EXACT, false>(p, ops, s); return true; }
+            if (variant == 6) { launch_one<Ops, 1, 2, 1, 8, EXACT, false, 6>(p, ops, s); return true; }
+            if (variant == 0) { launch_one<Ops, 1, 2, 1, 8, EXACT, false>(p, ops, s); return true; }
+            launch_one<Ops, 1, 2, 1, 4, EXACT, false, 8>(p, ops, s); return true;  // config 4
         case 4: launch_one<Ops, 1, 4, 1, 8, EXACT, false>(p, ops, s); return true;
         case 8: launch_one<Ops, 2, 4, 1, 8, EXACT, false>(p, ops, s); return true;
         case 16: launch_one<Ops, 4, 4, 1, 8, EXACT, false>(p, ops, s); return true;
@@ -41,6 +41,9 @@ inline bool launch_aligned(const KParams& p, const Ops& ops, int d, int variant,
                 if (variant == 3) { launch_one<Ops, 8, 4, 1, 16, EXACT, false>(p, ops, s); return true; }
                 if (variant == 4) { launch_one<Ops, 4, 4, 2, 8, EXACT, false>(p, ops, s); return true; }
                 if (variant == 5) { launch_one<Ops, 2, 4, 4, 2, EXACT, false>(p, ops, s); return true; }
+                if (variant == 1) { launch_one<Ops, 4, 4, 2, 4, EXACT, false>(p, ops, s); return true; }
+                if (variant == 7) { launch_one<Ops, 4, 4, 2, 8, EXACT, false, 3>(p, ops, s); return true; }
+                launch_one<Ops, 4, 4, 2, 4, EXACT, false, 4>(p, ops, s); return true;  // config 3
             }
             launch_one<Ops, 4, 4, 2, 4, EXACT, false>(p, ops, s); return true;
         case 64:
@@ -56,6 +59,8 @@ inline bool launch_aligned(const KParams& p, const Ops& ops, int d, int variant,
                 if (variant == 3) { launch_one<Ops, 16, 4, 2, 4, EXACT, false>(p, ops, s); return true; }
                 if (variant == 4) { launch_one<Ops, 4, 4, 8, 2, EXACT, false>(p, ops, s); return true; }
                 if (variant == 5) { launch_one<Ops, 8, 4, 4, 8, EXACT, false>(p, ops, s); return true; }
+                if (variant == 6) { launch_one<Ops, 8, 4, 4, 4, EXACT, false, 3>(p, ops, s); return true; }
+                if (variant == 7) { launch_one<Ops, 8, 4, 4, 2, EXACT, false, 4>(p, ops, s); return true; }
                 launch_one<Ops, 8, 4, 4, 4, EXACT, false>(p, ops, s); return true;
             }
             launch_one<Ops, 8, 4, 4, 2, EXACT, false>(p, ops, s); return true;
@@ -63,6 +68,8 @@ inline bool launch_aligned(const KParams& p, const Ops& ops, int d, int variant,
             if constexpr (!EXACT) {
                 if (variant == 0) { launch_one<Ops, 32, 4, 2, 4, EXACT, false>(p, ops, s); return true; }
                 if (variant == 2) { launch_one<Ops, 8, 4, 8, 1, EXACT, false>(p, ops, s); return true; }
+                if (variant == 6) { launch_one<Ops, 16, 4, 4, 2, EXACT, false, 2>(p, ops, s); return true; }
+                if (variant == 7) { launch_one<Ops, 16, 4, 4, 4, EXACT, false>(p, ops, s); return true; }
             }
             launch_one<Ops, 16, 4, 4, 2, EXACT, false>(p, ops, s); return true;
         case 512: launch_one<Ops, 32, 4, 4, 2, EXACT, false>(p, ops, s); return true;

@@ -419,8 +419,10 @@ __device__ __forceinline__ void gather_rows(const float* __restrict__ Y, int d, 
 // (edge k -> group k % GPW), each group folds its edges in storage order,
 // and the GPW partial z are combined by an xor-butterfly in fixed order.
 // Lane layout: element j = (i*LPG + lane_in_group)*VEC + c.
-template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED>
-__global__ void __launch_bounds__(256)
+// MINB = 0 leaves the register budget to ptxas (as __launch_bounds__(256));
+// MINB > 0 asks for that many resident blocks per SM (tuning variants).
+template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED, int MINB = 0>
+__global__ void __launch_bounds__(256, MINB)
 fmm_rows_kernel(const KParams p, const Ops ops) {
     constexpr int NE = NV * VEC;
     constexpr int GPW = 32 / LPG;
