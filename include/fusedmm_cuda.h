@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define FMM_ABI_VERSION 1
+#define FMM_ABI_VERSION 2
 
 /* Status codes. FMM_E_INVAL maps to std::invalid_argument and FMM_E_LOGIC to
  * std::logic_error in the C++ wrapper (kernel.hpp:272-281,303; ops.hpp:102-103). */
@@ -49,7 +49,10 @@ typedef enum fmm_status {
  * USER VOP lambda (SURVEY.md §8(a) "Oracle op definitions"). */
 enum {
     FMM_VOP_ADD = 0, FMM_VOP_MUL = 1, FMM_VOP_SEL2ND = 2, FMM_VOP_SUB = 3,
-    FMM_VOP_USER = 4
+    FMM_VOP_USER = 4,
+    FMM_VOP_MLP = 16 /* t_j = sigmoid(mlp_wx*x_j + mlp_wy*y_j + mlp_b): the
+                        reference's toy single-layer MLP hook for GNN_MLP
+                        (apps.hpp:58-64) as a device op                    */
 };
 enum {
     FMM_ROP_NOOP = 0, FMM_ROP_RSUM = 1, FMM_ROP_RMUL = 2, FMM_ROP_NORM = 3,
@@ -82,6 +85,7 @@ typedef struct fmm_opspec {
     int32_t vop, rop, sop, mop, aop;
     float alpha; /* SCAL factor (ops.hpp:49)                  */
     float k;     /* SQK divisor; ignored by the other ops      */
+    float mlp_wx, mlp_wy, mlp_b; /* FMM_VOP_MLP weights and bias   */
 } fmm_opspec;
 
 /* fmm_run / fmm_iterate flags. */

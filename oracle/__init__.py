@@ -31,12 +31,15 @@ PD = C.POINTER(C.c_double)
 
 class or_spec(C.Structure):
     _fields_ = [("vop", C.c_int32), ("rop", C.c_int32), ("sop", C.c_int32), ("mop", C.c_int32),
-                ("aop", C.c_int32), ("alpha", C.c_double), ("k", C.c_double)]
+                ("aop", C.c_int32), ("alpha", C.c_double), ("k", C.c_double),
+                ("mlp_wx", C.c_double), ("mlp_wy", C.c_double), ("mlp_b", C.c_double)]
 
 
 def _spec(spec) -> or_spec:
+    f = lambda v: float(np.float32(v))  # noqa: E731 — the reference's T=float parameters
     return or_spec(int(spec.vop), int(spec.rop), int(spec.sop), int(spec.mop), int(spec.aop),
-                   float(np.float32(spec.alpha)), float(np.float32(spec.k)))
+                   f(spec.alpha), f(spec.k), f(getattr(spec, "mlp_wx", 0.0)), f(getattr(spec, "mlp_wy", 0.0)),
+                   f(getattr(spec, "mlp_b", 0.0)))
 
 
 _or = None

@@ -32,7 +32,8 @@
 #include <stdlib.h>
 #include <string.h>
 
-enum { OR_VOP_ADD = 0, OR_VOP_MUL = 1, OR_VOP_SEL2ND = 2, OR_VOP_SUB = 3, OR_VOP_USER = 4 };
+enum { OR_VOP_ADD = 0, OR_VOP_MUL = 1, OR_VOP_SEL2ND = 2, OR_VOP_SUB = 3, OR_VOP_USER = 4,
+       OR_VOP_MLP = 16 };
 enum { OR_ROP_NOOP = 0, OR_ROP_RSUM = 1, OR_ROP_RMUL = 2, OR_ROP_NORM = 3, OR_ROP_USER = 4,
        OR_ROP_SQNORM = 16 };
 enum { OR_SOP_NOOP = 0, OR_SOP_SIGMOID = 1, OR_SOP_SCAL = 2, OR_SOP_USER = 3, OR_SOP_TDIST = 16,
@@ -51,6 +52,7 @@ typedef struct {
     int32_t vop, rop, sop, mop, aop;
     double alpha;
     double k;
+    double mlp_wx, mlp_wy, mlp_b; /* OR_VOP_MLP: apps.hpp:58-64 toy hook */
 } or_spec;
 
 typedef struct {

@@ -8,10 +8,15 @@
 /* ops.hpp:53-56 — exact sigmoid, no LUT, no clamp */
 static REAL SFX(sigmoid)(REAL s) { return (REAL)1 / ((REAL)1 + EXPF(-s)); }
 
-/* ops.hpp:58-80 */
-static void SFX(apply_vop)(int vop, const REAL* x, const REAL* y, REAL* out, int64_t d) {
+/* ops.hpp:58-80; OR_VOP_MLP is make_toy_mlp_vop (apps.hpp:58-64):
+ * sigmoid(w_x*x + w_y*y + bias), left to right */
+static void SFX(apply_vop)(const or_spec* sp, const REAL* x, const REAL* y, REAL* out, int64_t d) {
     int64_t i;
-    switch (vop) {
+    switch (sp->vop) {
+        case OR_VOP_MLP:
+            for (i = 0; i < d; ++i)
+                out[i] = SFX(sigmoid)((REAL)sp->mlp_wx * x[i] + (REAL)sp->mlp_wy * y[i] + (REAL)sp->mlp_b);
+            break;
         case OR_VOP_ADD: for (i = 0; i < d; ++i) out[i] = x[i] + y[i]; break;
         case OR_VOP_MUL: for (i = 0; i < d; ++i) out[i] = x[i] * y[i]; break;
         case OR_VOP_SEL2ND: for (i = 0; i < d; ++i) out[i] = y[i]; break;
@@ -69,20 +74,20 @@ static void SFX(update_u)(const int64_t* cols, const REAL* vals, int64_t nk, con
         const REAL a = vals ? vals[k] : (REAL)1;
         if (sp->mop == OR_MOP_MUL_VOP && sp->rop != OR_ROP_NOOP) {
             REAL s, h;
-            SFX(apply_vop)(sp->vop, x_u, y_v, tmp, d);
+            SFX(apply_vop)(sp, x_u, y_v, tmp, d);
             s = SFX(apply_rop)(sp->rop, tmp, d);
             h = SFX(apply_sop)(sp, s);
             for (j = 0; j < d; ++j) tmp[j] = h * tmp[j];
             for (j = 0; j < d; ++j) w[j] = a * tmp[j];
         } else if (sp->rop != OR_ROP_NOOP) { /* scalar message, ops.hpp:45 */
             REAL s, h;
-            SFX(apply_vop)(sp->vop, x_u, y_v, tmp, d);
+            SFX(apply_vop)(sp, x_u, y_v, tmp, d);
             s = SFX(apply_rop)(sp->rop, tmp, d);
             h = SFX(apply_sop)(sp, s);
             if (sp->mop == OR_MOP_SEL2ND) for (j = 0; j < d; ++j) w[j] = y_v[j];
             else for (j = 0; j < d; ++j) w[j] = h * y_v[j]; /* a_uv ignored, ops.hpp:131-137 */
         } else { /* vector message */
-            SFX(apply_vop)(sp->vop, x_u, y_v, tmp, d);
+            SFX(apply_vop)(sp, x_u, y_v, tmp, d);
             if (sp->sop != OR_SOP_NOOP)
                 for (j = 0; j < d; ++j) tmp[j] = SFX(apply_sop)(sp, tmp[j]);
             if (sp->mop == OR_MOP_SEL2ND) for (j = 0; j < d; ++j) w[j] = y_v[j];

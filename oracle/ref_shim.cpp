@@ -33,7 +33,10 @@ struct RefSpec {
     int32_t vop, rop, sop, mop, aop;
     double alpha;
     double k;
+    double mlp_wx, mlp_wy, mlp_b;
 };
+
+enum { EXT_VOP_MLP = 16 };
 
 enum { EXT_ROP_SQNORM = 16, EXT_SOP_TDIST = 16, EXT_SOP_SQK = 17, EXT_MOP_MUL_VOP = 16 };
 
@@ -65,6 +68,12 @@ OpSpec<T> make_ref_spec(const RefSpec& s) {
         return spec;
     }
     spec.vop = static_cast<Vop>(s.vop);
+    if (s.vop == EXT_VOP_MLP) {
+        // the reference's own toy MLP hook (apps.hpp:58-64) as a USER VOP
+        spec.vop = Vop::USER;
+        spec.user_vop = make_toy_mlp_vop<T>(static_cast<T>(s.mlp_wx), static_cast<T>(s.mlp_wy),
+                                            static_cast<T>(s.mlp_b));
+    }
     spec.rop = static_cast<Rop>(s.rop);
     spec.sop = static_cast<Sop>(s.sop);
     spec.mop = static_cast<Mop>(s.mop);

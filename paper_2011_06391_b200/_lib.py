@@ -27,7 +27,8 @@ FMM_EXCHANGE_COPIES = 1 << 4
 
 class fmm_opspec(C.Structure):
     _fields_ = [("vop", C.c_int32), ("rop", C.c_int32), ("sop", C.c_int32),
-                ("mop", C.c_int32), ("aop", C.c_int32), ("alpha", C.c_float), ("k", C.c_float)]
+                ("mop", C.c_int32), ("aop", C.c_int32), ("alpha", C.c_float), ("k", C.c_float),
+                ("mlp_wx", C.c_float), ("mlp_wy", C.c_float), ("mlp_b", C.c_float)]
 
 
 class fmm_stats(C.Structure):

@@ -143,7 +143,7 @@ bool is_user(const fmm_opspec& s) {
 }
 
 bool valid_codes(const fmm_opspec& s) {
-    const bool v = s.vop >= FMM_VOP_ADD && s.vop <= FMM_VOP_USER;
+    const bool v = (s.vop >= FMM_VOP_ADD && s.vop <= FMM_VOP_USER) || s.vop == FMM_VOP_MLP;
     const bool r = (s.rop >= FMM_ROP_NOOP && s.rop <= FMM_ROP_USER) || s.rop == FMM_ROP_SQNORM;
     const bool so = (s.sop >= FMM_SOP_NOOP && s.sop <= FMM_SOP_USER) || s.sop == FMM_SOP_TDIST ||
                     s.sop == FMM_SOP_SQK;
@@ -251,6 +251,9 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
     p.vop = spec.vop; p.rop = spec.rop; p.sop = spec.sop; p.mop = spec.mop; p.aop = spec.aop;
     p.alpha = spec.alpha;
     p.k = spec.k;
+    p.mlp_wx = spec.mlp_wx;
+    p.mlp_wy = spec.mlp_wy;
+    p.mlp_b = spec.mlp_b;
     const int64_t rows = gs.row_end - gs.row_begin;
     const bool split = !exact && gs.n_chunks > 0;
     if (!exact) {

@@ -35,7 +35,7 @@ static bool generic_masked(const KParams& p, const DOps& ops, int d, cudaStream_
 }
 
 bool launch_generic(const KParams& p, int d, bool exact, bool vectorised, cudaStream_t s) {
-    const DOps ops{p.vop, p.rop, p.sop, p.mop, p.aop};
+    const DOps ops{p.vop, p.rop, p.sop, p.mop, p.aop, p.mlp_wx, p.mlp_wy, p.mlp_b};
     if (vectorised)
         return exact ? generic_aligned<true>(p, ops, d, s) : generic_aligned<false>(p, ops, d, s);
     return exact ? generic_masked<true>(p, ops, d, s) : generic_masked<false>(p, ops, d, s);

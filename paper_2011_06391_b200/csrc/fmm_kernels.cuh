@@ -57,6 +57,7 @@ struct KParams {
     // dynamic op codes (used by DOps only)
     int vop, rop, sop, mop, aop;
     float alpha, k;
+    float mlp_wx, mlp_wy, mlp_b;
     // fused exchange: every final z row is also stored to zpeer[q] + r*d —
     // the other shards' next-iterate buffers, reached over NVLink (P2P) — so
     // the per-iteration all-gather rides on the kernel's own stores
@@ -72,14 +73,17 @@ struct SOps {
     __device__ __forceinline__ int sop() const { return S; }
     __device__ __forceinline__ int mop() const { return M; }
     __device__ __forceinline__ int aop() const { return A; }
+    __device__ __forceinline__ float3 mlp() const { return make_float3(0.f, 0.f, 0.f); }
 };
 struct DOps {
     int v, r, s, m, a;
+    float wx, wy, wb;  // FMM_VOP_MLP weights / bias
     __device__ __forceinline__ int vop() const { return v; }
     __device__ __forceinline__ int rop() const { return r; }
     __device__ __forceinline__ int sop() const { return s; }
     __device__ __forceinline__ int mop() const { return m; }
     __device__ __forceinline__ int aop() const { return a; }
+    __device__ __forceinline__ float3 mlp() const { return make_float3(wx, wy, wb); }
 };
 
 using OpsSigmoid = SOps<FMM_VOP_MUL, FMM_ROP_RSUM, FMM_SOP_SIGMOID, FMM_MOP_MUL, FMM_AOP_ASUM>;
@@ -111,13 +115,34 @@ __device__ __forceinline__ float fmac(float acc, float a, float b) {
     else return fmaf(a, b, acc);
 }
 
-// ops.hpp:58-80
+// 1/x for x >= 1 (x may be +inf): rcp.approx refined by one Newton step,
+// branch-free, within 1 ulp of the IEEE quotient.
+__device__ __forceinline__ float recip_ge1(float x) {
+    x = fminf(x, 3.0e38f);  // 1/inf -> 0 without a NaN from the Newton step
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return fmaf(r, fmaf(-x, r, 1.0f), r);
+}
+
+template <bool EXACT>
+__device__ __forceinline__ float sigmoid_f(float s) {
+    if constexpr (EXACT) return 1.0f / (1.0f + expf(-s));
+    else return recip_ge1(1.0f + expf(-s));
+}
+
+// ops.hpp:58-80, plus the toy MLP hook of apps.hpp:58-64 as FMM_VOP_MLP:
+// sigmoid(w_x*x + w_y*y + bias), evaluated left to right without contraction
+// on the exact scheme
 template <bool EXACT, class Ops>
 __device__ __forceinline__ float vop_apply(const Ops& ops, float x, float y) {
     switch (ops.vop()) {
         case FMM_VOP_ADD: return fadd<EXACT>(x, y);
         case FMM_VOP_MUL: return fmul<EXACT>(x, y);
         case FMM_VOP_SEL2ND: return y;
+        case FMM_VOP_MLP: {
+            const float3 w = ops.mlp();
+            return sigmoid_f<EXACT>(fadd<EXACT>(fadd<EXACT>(fmul<EXACT>(w.x, x), fmul<EXACT>(w.y, y)), w.z));
+        }
         default: return fsub<EXACT>(x, y);  // FMM_VOP_SUB
     }
 }
@@ -143,24 +168,13 @@ __device__ __forceinline__ float vop_rop_step(const Ops& ops, float acc, float x
     return rop_step<EXACT>(ops, acc, vop_apply<EXACT>(ops, x, y));
 }
 
-// 1/x for x >= 1 (x may be +inf): rcp.approx refined by one Newton step,
-// branch-free, within 1 ulp of the IEEE quotient.
-__device__ __forceinline__ float recip_ge1(float x) {
-    x = fminf(x, 3.0e38f);  // 1/inf -> 0 without a NaN from the Newton step
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return fmaf(r, fmaf(-x, r, 1.0f), r);
-}
-
 // ops.hpp:53-56, 108-121 plus the device extensions TDIST / SQK. Sigmoid is
 // 1/(1+exp(-s)) with CUDA's accurate expf (no LUT, no clamp);
 // the exact scheme divides with IEEE rounding, the fast one uses recip_ge1.
 template <bool EXACT, class Ops>
 __device__ __forceinline__ float sop_apply(const Ops& ops, float s, float alpha, float k) {
     switch (ops.sop()) {
-        case FMM_SOP_SIGMOID:
-            if constexpr (EXACT) return 1.0f / (1.0f + expf(-s));
-            else return recip_ge1(1.0f + expf(-s));
+        case FMM_SOP_SIGMOID: return sigmoid_f<EXACT>(s);
         case FMM_SOP_SCAL: return __fmul_rn(alpha, s);
         case FMM_SOP_TDIST:
             // s >= 0 after a squared / plain norm, so 1+s >= 1
@@ -254,7 +268,7 @@ __device__ __forceinline__ void consume_edges(const Ops& ops, const KParams& p, 
         // instruction), fast scheme only: scalar messages with ASUM. (The
         // exact scheme stays scalar: ptxas may contract packed mul+add.)
         if (!EXACT && ops.aop() == FMM_AOP_ASUM && ops.rop() != FMM_ROP_NOOP &&
-            ops.rop() != FMM_ROP_RMUL && ops.mop() != FMM_MOP_SEL2ND) {
+            ops.rop() != FMM_ROP_RMUL && ops.mop() != FMM_MOP_SEL2ND && ops.vop() != FMM_VOP_MLP) {
             float s[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {

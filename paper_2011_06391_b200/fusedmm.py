@@ -81,6 +81,7 @@ class Vop(enum.IntEnum):
     SEL2ND = 2
     SUB = 3
     USER = 4
+    MLP = 16  # device op: sigmoid(mlp_wx*x + mlp_wy*y + mlp_b) (apps.hpp:58-64)
 
 
 class Rop(enum.IntEnum):
@@ -134,6 +135,9 @@ class OpSpec:
     aop: Aop = Aop.ASUM
     alpha: float = 1.0
     k: float = 1.0
+    mlp_wx: float = 0.0
+    mlp_wy: float = 0.0
+    mlp_b: float = 0.0
     user_vop: Optional[Callable] = None
     user_rop: Optional[Callable] = None
     user_sop: Optional[Callable] = None
@@ -149,7 +153,8 @@ class OpSpec:
 
     def to_c(self) -> fmm_opspec:
         return fmm_opspec(int(self.vop), int(self.rop), int(self.sop), int(self.mop),
-                          int(self.aop), float(self.alpha), float(self.k))
+                          int(self.aop), float(self.alpha), float(self.k), float(self.mlp_wx),
+                          float(self.mlp_wy), float(self.mlp_b))
 
 
 def pattern_of(spec: OpSpec) -> KnownPattern:
@@ -621,8 +626,34 @@ def make_spec(app: App, params: Optional[AppParams] = None) -> OpSpec:
     if app == App.GNN_MLP:
         if params.mlp_vop is None:
             raise InvalidArgument("make_spec: GNN_MLP needs a user-provided MLP function")
+        if isinstance(params.mlp_vop, ToyMLP):
+            # the toy hook has a device op; any other callable stays a USER slot
+            m = params.mlp_vop
+            return OpSpec(Vop.MLP, Rop.NOOP, Sop.SIGMOID, Mop.MUL, Aop.AMAX, mlp_wx=m.w_x, mlp_wy=m.w_y,
+                          mlp_b=m.bias)
         return OpSpec(Vop.USER, Rop.NOOP, Sop.SIGMOID, Mop.MUL, Aop.AMAX, user_vop=params.mlp_vop)
     raise InvalidArgument("make_spec: unknown app")
+
+
+@dataclass
+class ToyMLP:
+    """make_toy_mlp_vop (apps.hpp:58-64): out[j] = sigmoid(w_x*x[j] + w_y*y[j]
+    + bias). Callable like the reference lambda, and recognised by make_spec
+    as the device op Vop.MLP."""
+    w_x: float
+    w_y: float
+    bias: float
+
+    def __call__(self, x, y, out):
+        x = np.asarray(x, np.float32)
+        y = np.asarray(y, np.float32)
+        pre = (np.float32(self.w_x) * x + np.float32(self.w_y) * y) + np.float32(self.bias)
+        out[:] = (np.float32(1) / (np.float32(1) + np.exp(-pre))).astype(np.float32)
+
+
+def make_toy_mlp_vop(w_x: float, w_y: float, bias: float) -> ToyMLP:
+    """apps.hpp:58-64."""
+    return ToyMLP(w_x, w_y, bias)
 
 
 def fr_layout_sub_spec(alpha: float) -> OpSpec:

@@ -32,7 +32,8 @@ def save(name, A, X, Y, spec, lane_width=8, t=3):
         values=A.values, unit=bool(getattr(A, "unit_values", False)), X=X.array,
         Y=Y.array, y_is_x=Y is X,
         spec=np.array([int(spec.vop), int(spec.rop), int(spec.sop), int(spec.mop), int(spec.aop)]),
-        alpha=np.float32(spec.alpha), k=np.float32(spec.k), lane_width=lane_width, Z=Z)
+        alpha=np.float32(spec.alpha), k=np.float32(spec.k),
+        mlp=np.array([spec.mlp_wx, spec.mlp_wy, spec.mlp_b], np.float32), lane_width=lane_width, Z=Z)
     print(name, A.nrows, A.nnz(), X.dim, float(np.abs(Z[np.isfinite(Z)]).max(initial=0)))
 
 
@@ -58,6 +59,7 @@ def main():
         "frattr": F.fr_attract_spec(1.0),
         "amax_rmul": F.OpSpec(F.Vop.ADD, F.Rop.RMUL, F.Sop.SCAL, F.Mop.SEL2ND, F.Aop.AMAX, alpha=0.7),
         "vecmsg_sigmoid_amax": F.OpSpec(F.Vop.MUL, F.Rop.NOOP, F.Sop.SIGMOID, F.Mop.MUL, F.Aop.AMAX),
+        "gnn_mlp": F.make_spec(F.App.GNN_MLP, F.AppParams(mlp_vop=F.make_toy_mlp_vop(0.3, 0.7, 0.1))),
     }
     for name, spec in specs.items():
         for d in (2, 16, 64):

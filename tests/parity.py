@@ -18,6 +18,22 @@ TOL = 1e-5
 TWO_TIER = 5e-6
 
 
+def load_golden(path):
+    """(A, X, Y, spec, lane_width, Z) of a tests/golden/*.npz fixture."""
+    from paper_2011_06391_b200 import fusedmm as F
+    g = np.load(path)
+    A = F.CsrMatrix(int(g["m"]), int(g["n"]), g["row_ptr"], g["col_idx"],
+                    None if bool(g["unit"]) else g["values"])
+    X = F.DenseMatrix.wrap(g["X"])
+    Y = X if bool(g["y_is_x"]) else F.DenseMatrix.wrap(g["Y"])
+    s = g["spec"]
+    mlp = g["mlp"] if "mlp" in g.files else np.zeros(3, np.float32)
+    spec = F.OpSpec(F.Vop(int(s[0])), F.Rop(int(s[1])), F.Sop(int(s[2])), F.Mop(int(s[3])), F.Aop(int(s[4])),
+                    alpha=float(g["alpha"]), k=float(g["k"]), mlp_wx=float(mlp[0]), mlp_wy=float(mlp[1]),
+                    mlp_b=float(mlp[2]))
+    return A, X, Y, spec, int(g["lane_width"]), g["Z"]
+
+
 def check_exact(Z_gpu: np.ndarray, Z_ref: np.ndarray) -> None:
     a = np.ascontiguousarray(Z_gpu, np.float32).view(np.uint32)
     b = np.ascontiguousarray(Z_ref, np.float32).view(np.uint32)

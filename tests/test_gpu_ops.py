@@ -94,24 +94,33 @@ def test_all_op_combinations_exact_thread_per_row(d):
 
 @pytest.mark.parametrize("path", sorted(GOLDEN.glob("*.npz")), ids=lambda p: p.stem)
 def test_golden_vectors_on_device(path):
-    g = np.load(path)
-    A = F.CsrMatrix(int(g["m"]), int(g["n"]), g["row_ptr"], g["col_idx"],
-                    None if bool(g["unit"]) else g["values"])
-    X = F.DenseMatrix.wrap(g["X"])
-    Y = X if bool(g["y_is_x"]) else F.DenseMatrix.wrap(g["Y"])
-    s = g["spec"]
-    spec = F.OpSpec(F.Vop(int(s[0])), F.Rop(int(s[1])), F.Sop(int(s[2])), F.Mop(int(s[3])), F.Aop(int(s[4])),
-                    alpha=float(g["alpha"]), k=float(g["k"]))
+    from tests.parity import load_golden
+    A, X, Y, spec, _lw, Zg = load_golden(path)
     st = F.KernelStats()
     Z = F.fused_mm(A, X, Y, spec, 1, st)
     if st.exact and (F.pattern_of(spec) == F.KnownPattern.SPMM_GCN or X.dim <= 4):
-        check_exact(Z.array, g["Z"])
+        check_exact(Z.array, Zg)
     else:
-        if np.all(np.isfinite(g["Z"])):
-            if np.abs(g["Z"]).max() > 0:
+        if np.all(np.isfinite(Zg)):
+            if np.abs(Zg).max() > 0:
                 loose_check(Z.array, A, X, Y, spec)
         else:
-            assert np.array_equal(np.isfinite(Z.array), np.isfinite(g["Z"]))
+            assert np.array_equal(np.isfinite(Z.array), np.isfinite(Zg))
+
+
+def test_every_make_spec_row_runs_on_device():
+    """apps.hpp:22-45: FR_LAYOUT, NODE_EMBED_SIGMOID, GCN_FORWARD and GNN_MLP
+    (with the toy MLP hook as the device op Vop.MLP) all run on the GPU."""
+    A, X, Y = random_case(77, 60, 60, 32, weighted=True)
+    mlp = F.AppParams(alpha=0.5, mlp_vop=F.make_toy_mlp_vop(0.4, 0.6, 0.1))
+    for app in (F.App.FR_LAYOUT, F.App.NODE_EMBED_SIGMOID, F.App.GCN_FORWARD, F.App.GNN_MLP):
+        spec = F.make_spec(app, mlp)
+        assert not spec.has_user_slot()
+        Z = F.fused_mm(A, X, Y, spec, 1)
+        loose_check(Z.array, A, X, Y, spec)
+        if oracle.ref_available():  # the reference itself, through its own toy hook
+            Zr = oracle.ref_fused_mm(A, X, Y, spec)
+            assert np.max(np.abs(Z.array - Zr)) <= 1e-5 * max(1.0, float(np.abs(Zr).max()))
 
 
 def test_empty_rows_and_amax_identity():

@@ -196,16 +196,10 @@ def golden_cases():
 
 @pytest.mark.parametrize("path", golden_cases(), ids=lambda p: p.stem)
 def test_oracle_matches_reference_golden(path):
-    g = np.load(path)
-    A = F.CsrMatrix(int(g["m"]), int(g["n"]), g["row_ptr"], g["col_idx"],
-                    None if bool(g["unit"]) else g["values"])
-    X = F.DenseMatrix.wrap(g["X"])
-    Y = X if bool(g["y_is_x"]) else F.DenseMatrix.wrap(g["Y"])
-    s = g["spec"]
-    spec = F.OpSpec(F.Vop(int(s[0])), F.Rop(int(s[1])), F.Sop(int(s[2])), F.Mop(int(s[3])), F.Aop(int(s[4])),
-                    alpha=float(g["alpha"]), k=float(g["k"]))
-    Z = run(A, X, Y, spec, lane_width=int(g["lane_width"]))
-    assert np.array_equal(Z.view(np.uint32), g["Z"].view(np.uint32)), path.stem
+    from tests.parity import load_golden
+    A, X, Y, spec, lw, Zg = load_golden(path)
+    Z = run(A, X, Y, spec, lane_width=lw)
+    assert np.array_equal(Z.view(np.uint32), Zg.view(np.uint32)), path.stem
 
 
 def test_golden_set_present():
@@ -222,6 +216,8 @@ SPECS = [
     F.OpSpec(F.Vop.ADD, F.Rop.RMUL, F.Sop.SCAL, F.Mop.SEL2ND, F.Aop.AMAX, alpha=0.7),
     F.OpSpec(F.Vop.MUL, F.Rop.NOOP, F.Sop.SIGMOID, F.Mop.MUL, F.Aop.AMAX),
     F.OpSpec(F.Vop.SUB, F.Rop.NORM, F.Sop.NOOP, F.Mop.MUL, F.Aop.ASUM),
+    # GNN_MLP with the reference's toy hook (apps.hpp:22-45, 58-64)
+    F.make_spec(F.App.GNN_MLP, F.AppParams(mlp_vop=F.make_toy_mlp_vop(0.4, 0.6, 0.1))),
 ]
 
 
