@@ -182,6 +182,17 @@ fmm_status fmm_run(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec,
 /* iters fused calls with X <- Z between them (square A, Y = X), the Z slices
  * exchanged between shards on the device. X is the host m x d input and
  * receives the final iterate. */
+/* The UNFUSED baseline of the same call (reference.hpp:41-155 on the
+ * device): an SDDMM kernel materialises the per-edge messages H (nnz
+ * scalars, or nnz*d values for vector messages) in HBM, then an SpMM pass
+ * aggregates them. Device pointers, single-shard context, d in
+ * {32, 64, 128, 256}; stats->aux_bytes = bytes of H. For measuring what the
+ * fusion saves, not for production use. */
+fmm_status fmm_run_unfused(fmm_ctx* ctx, const fmm_graph* g,
+                           const fmm_opspec* spec, int64_t d, const float* X,
+                           int64_t ny, const float* Y, float* Z,
+                           uint32_t flags, fmm_stats* stats);
+
 /* Wait for every call enqueued with FMM_ASYNC on this context. */
 fmm_status fmm_sync(fmm_ctx* ctx);
 

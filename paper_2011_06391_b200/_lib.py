@@ -70,6 +70,8 @@ SIGNATURES = {
     "fmm_iterate": (C.c_int, [_P, _P, C.POINTER(fmm_opspec), C.c_int64, _P, C.c_int,
                               C.c_uint32, C.POINTER(fmm_stats)]),
     "fmm_sync": (C.c_int, [_P]),
+    "fmm_run_unfused": (C.c_int, [_P, _P, C.POINTER(fmm_opspec), C.c_int64, _P, C.c_int64, _P, _P,
+                                  C.c_uint32, C.POINTER(fmm_stats)]),
     "fmm_host_alloc": (C.c_int, [C.POINTER(_P), C.c_size_t]),
     "fmm_host_free": (C.c_int, [_P]),
 }

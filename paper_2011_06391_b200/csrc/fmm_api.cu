@@ -11,6 +11,7 @@
 #include "fmm_dispatch.cuh"
 #include "fmm_plan.h"
 #include "fmm_sched.cuh"
+#include "fmm_unfused.h"
 
 #include <algorithm>
 #include <cstdlib>
@@ -37,6 +38,7 @@ struct Shard {
     cudaStream_t ext = nullptr;
     bool use_ext = false;  // ext may legitimately be the legacy NULL stream
     DevBuf X, Y, Z, Xb, partial;
+    DevBuf H, iota;  // unfused baseline: materialised messages, edge ids
     cudaEvent_t ev_start = nullptr, ev_k0 = nullptr, ev_k1 = nullptr, ev_end = nullptr,
                 ev_copy = nullptr;
     // host-pointer FMM_ASYNC pipeline: two buffer slots, copy-in / compute /
@@ -544,7 +546,7 @@ fmm_status fmm_destroy(fmm_ctx* ctx) {
         if (sh.own) cudaStreamSynchronize(sh.own);
         for (cudaStream_t st : {sh.s_in, sh.s_out})
             if (st) cudaStreamSynchronize(st);
-        for (DevBuf* b : {&sh.X, &sh.Y, &sh.Z, &sh.Xb, &sh.partial, &sh.aX[0], &sh.aX[1], &sh.aY[0],
+        for (DevBuf* b : {&sh.X, &sh.Y, &sh.Z, &sh.Xb, &sh.partial, &sh.H, &sh.iota, &sh.aX[0], &sh.aX[1], &sh.aY[0],
                           &sh.aY[1], &sh.aZ[0], &sh.aZ[1]})
             if (b->ptr) cudaFree(b->ptr);
         for (cudaEvent_t e : {sh.ev_start, sh.ev_k0, sh.ev_k1, sh.ev_end, sh.ev_copy, sh.ev_in[0], sh.ev_in[1],
@@ -849,6 +851,102 @@ fmm_status fmm_run(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec, int
         stats->total_ms = tms;
     }
     (void)rows;
+    return FMM_OK;
+}
+
+fmm_status fmm_run_unfused(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec, int64_t d,
+                           const float* X, int64_t ny, const float* Y, float* Z, uint32_t flags,
+                           fmm_stats* stats) {
+    if (!ctx || !g || g->ctx != ctx) return FMM_E_INVAL;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    fmm_status st = check_spec(ctx, spec, d);
+    if (st != FMM_OK) return st;
+    if (!(flags & FMM_DEVICE_PTRS) || ctx->shards.size() != 1)
+        return set_err(ctx, FMM_E_INVAL, "unfused: device pointers on a single-shard context");
+    if (spec->mop == FMM_MOP_MUL_VOP || spec->vop == FMM_VOP_MLP)
+        return set_err(ctx, FMM_E_UNSUPPORTED, "unfused: op not in the reference's unfused pipeline");
+    if (d != 32 && d != 64 && d != 128 && d != 256)
+        return set_err(ctx, FMM_E_UNSUPPORTED, "unfused: d must be 32, 64, 128 or 256");
+    if (g->nnz > 0 && ny < g->max_col + 1) return set_err(ctx, FMM_E_INVAL, "fused_mm: Y has too few rows");
+    const GShard& gs = g->shards[0];
+    Shard& sh = ctx->shards[gs.shard];
+    FMM_CK(ctx, cudaSetDevice(sh.dev));
+    cudaStream_t stream = sh.stream();
+    const bool scalar = spec->rop != FMM_ROP_NOOP;
+    const int64_t rows = gs.row_end - gs.row_begin;
+    const size_t hbytes = std::max<size_t>(1, static_cast<size_t>(gs.nnz) * (scalar ? 1 : d) * sizeof(float));
+    if ((st = ensure(ctx, sh, sh.H, hbytes)) != FMM_OK) return st;
+    size_t aux = hbytes;
+    const bool timed = stats != nullptr && !(flags & FMM_ASYNC);
+    if (timed) FMM_CK(ctx, cudaEventRecord(sh.ev_k0, stream));
+    // phase 1: SDDMM, H materialised in HBM
+    fmm::SddmmParams sp{};
+    sp.row_ptr = gs.row_ptr;
+    sp.col = gs.col;
+    sp.val = gs.val;
+    sp.X = X;
+    sp.Y = Y;
+    sp.H = static_cast<float*>(sh.H.ptr);
+    sp.order = gs.order;
+    sp.n_rows = rows;
+    sp.nnz = gs.nnz;
+    sp.row0 = gs.row_begin;
+    sp.d = static_cast<int>(d);
+    sp.alpha = spec->alpha;
+    sp.k = spec->k;
+    if (!fmm::launch_sddmm(sp, spec->vop, spec->rop, spec->sop, spec->mop, spec->aop, stream))
+        return set_err(ctx, FMM_E_UNSUPPORTED, "unfused: no SDDMM kernel");
+    FMM_CK(ctx, cudaGetLastError());
+    int launches = 1;
+    // phase 2: SpMM over the materialised messages with the row kernels
+    fmm_opspec sp2{FMM_VOP_SEL2ND, FMM_ROP_NOOP, FMM_SOP_NOOP, FMM_MOP_MUL, spec->aop, 1.f, 1.f, 0.f, 0.f, 0.f};
+    GShard g2 = gs;  // shallow: same device arrays, possibly other columns
+    const float* vals = gs.val;
+    const float* Ysrc = Y;
+    if (spec->mop == FMM_MOP_SEL2ND) {
+        vals = nullptr;  // w = y_v
+    } else if (scalar) {
+        vals = static_cast<const float*>(sh.H.ptr);  // w = h_e * y_v
+    } else {
+        // w = a_uv * H[e]: gather H rows by edge id
+        const size_t ib = std::max<size_t>(1, static_cast<size_t>(gs.nnz) * sizeof(int32_t));
+        if ((st = ensure(ctx, sh, sh.iota, ib)) != FMM_OK) return st;
+        fmm::launch_iota(static_cast<int32_t*>(sh.iota.ptr), gs.nnz, stream);
+        ++launches;
+        g2.col = static_cast<int32_t*>(sh.iota.ptr);
+        Ysrc = static_cast<const float*>(sh.H.ptr);
+        aux += ib;
+    }
+    float* part = nullptr;
+    if (gs.n_slots > 0) {
+        const size_t pb = static_cast<size_t>(gs.n_slots) * d * sizeof(float);
+        if ((st = ensure(ctx, sh, sh.partial, pb)) != FMM_OK) return st;
+        part = static_cast<float*>(sh.partial.ptr);
+    }
+    const int l = launch_shard(g2, sp2, pattern_of(sp2), d, /*exact=*/false, X, gs.row_begin, Ysrc, Z, part,
+                               vals, ctx->variant, sh.num_sms, stream);
+    g2.scheds.clear();
+    if (l < 0) return set_err(ctx, FMM_E_UNSUPPORTED, "unfused: no SpMM kernel");
+    launches += l;
+    FMM_CK(ctx, cudaGetLastError());
+    float kms = 0.f;
+    if (timed) {
+        FMM_CK(ctx, cudaEventRecord(sh.ev_k1, stream));
+        FMM_CK(ctx, cudaStreamSynchronize(stream));
+        kms = elapsed(sh.ev_k0, sh.ev_k1);
+    } else if (!(flags & FMM_ASYNC)) {
+        FMM_CK(ctx, cudaStreamSynchronize(stream));
+    }
+    if (stats) {
+        *stats = fmm_stats{};
+        stats->aux_bytes = aux;
+        stats->threads = 1;
+        stats->pattern = pattern_of(*spec);
+        stats->exact = 0;
+        stats->launches = launches;
+        stats->kernel_ms = kms;
+        stats->total_ms = kms;
+    }
     return FMM_OK;
 }
 

@@ -483,6 +483,15 @@ class DeviceGraph:
                                 C.byref(stats) if stats is not None else None)
         _raise(st, self.ctx.h)
 
+    def run_unfused_device(self, x_ptr: int, ny: int, y_ptr: int, z_ptr: int, d: int, spec: OpSpec,
+                           flags: int = _lib.FMM_DEVICE_PTRS) -> fmm_stats:
+        """The unfused SDDMM -> SpMM baseline (fmm_run_unfused)."""
+        s = fmm_stats()
+        st = _lib.lib().fmm_run_unfused(self.ctx.h, self.h, C.byref(spec.to_c()), d, C.c_void_p(x_ptr), ny,
+                                        C.c_void_p(y_ptr), C.c_void_p(z_ptr), flags, C.byref(s))
+        _raise(st, self.ctx.h)
+        return s
+
     def iterate_host(self, X: np.ndarray, d: int, spec: OpSpec, iters: int, flags: int = 0) -> fmm_stats:
         s = fmm_stats()
         st = _lib.lib().fmm_iterate(self.ctx.h, self.h, C.byref(spec.to_c()), d, _vp(X), iters, flags,
