@@ -442,6 +442,10 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
     constexpr int GPW = 32 / LPG;
     constexpr int U = UNROLL;
     static_assert(32 % LPG == 0, "group shape");
+    // Fetch column indices one batch ahead on the wide-row fast shapes
+    // (config 2: -5%, config 5: -1.5%); for short rows / small d the extra
+    // registers cost more than the hidden index latency (measured).
+    constexpr bool kPrefetchCols = !EXACT && !MASKED && (LPG * VEC * NV >= 128);
 
     const int lane = threadIdx.x & 31;
     const int gl = lane & (LPG - 1);
@@ -505,19 +509,32 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
         constexpr int KPL = B / 32;                   // column slots per lane
         static_assert(SB <= 32 ? (32 % SB == 0) : (SB % 32 == 0), "sub-batch shape");
         const int n = static_cast<int>(e1 - e0);
+        int cnext[KPL];
+        float anext[KPL];
+        auto fetch = [&](int bb) {  // one batch ahead, as in the narrow loop
+#pragma unroll
+            for (int q = 0; q < KPL; ++q) {
+                const int eb = bb + q * 32 + lane;
+                cnext[q] = 0;
+                anext[q] = 1.0f;
+                if (eb < n) {
+                    cnext[q] = ld_stream_i32(p.col + e0 + eb);
+                    if (has_val) anext[q] = ld_stream_f32(p.val + e0 + eb);
+                }
+            }
+        };
+        if constexpr (kPrefetchCols) fetch(0);
         for (int base = 0; base < n; base += B) {
+            if constexpr (!kPrefetchCols) fetch(base);
             int cidx[KPL];
             float aval[KPL];
 #pragma unroll
             for (int q = 0; q < KPL; ++q) {
-                const int eb = base + q * 32 + lane;
-                cidx[q] = 0;
-                aval[q] = 1.0f;
-                if (eb < n) {
-                    cidx[q] = ld_stream_i32(p.col + e0 + eb);
-                    if (has_val) aval[q] = ld_stream_f32(p.val + e0 + eb);
-                }
+                cidx[q] = cnext[q];
+                aval[q] = anext[q];
             }
+            if constexpr (kPrefetchCols)
+                if (base + B < n) fetch(base + B);
             const int cnt = min(B, n - base);
             // SB >= 32: a single sub-batch per column batch (static slots);
             // SB < 32: KPL == 1 and the sub-batch offset s is a run-time value.
@@ -573,19 +590,34 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
         constexpr int KPL = B / LPG;            // column slots per lane
         const int n = static_cast<int>(e1 - e0);
         const int nmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(n)));
+        // column indices are fetched one batch ahead, so the index load of
+        // batch k+1 overlaps the gathers of batch k instead of preceding them
+        int cnext[KPL];
+        float anext[KPL];
+        auto fetch = [&](int bb) {
+#pragma unroll
+            for (int q = 0; q < KPL; ++q) {
+                const int eb = bb + q * LPG + gl;
+                cnext[q] = 0;
+                anext[q] = 1.0f;
+                if (eb < n) {
+                    cnext[q] = ld_stream_i32(p.col + e0 + eb);
+                    if (has_val) anext[q] = ld_stream_f32(p.val + e0 + eb);
+                }
+            }
+        };
+        if constexpr (kPrefetchCols) fetch(0);
         for (int base = 0; base < nmax; base += B) {
+            if constexpr (!kPrefetchCols) fetch(base);
             int cidx[KPL];
             float aval[KPL];
 #pragma unroll
             for (int q = 0; q < KPL; ++q) {
-                const int eb = base + q * LPG + gl;
-                cidx[q] = 0;
-                aval[q] = 1.0f;
-                if (eb < n) {
-                    cidx[q] = ld_stream_i32(p.col + e0 + eb);
-                    if (has_val) aval[q] = ld_stream_f32(p.val + e0 + eb);
-                }
+                cidx[q] = cnext[q];
+                aval[q] = anext[q];
             }
+            if constexpr (kPrefetchCols)
+                if (base + B < nmax) fetch(base + B);
             const int cnt = min(B, nmax - base);  // warp-uniform
 #pragma unroll 1
             for (int u0 = 0; u0 < B; u0 += U) {
