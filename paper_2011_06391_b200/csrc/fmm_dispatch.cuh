@@ -69,7 +69,10 @@ inline bool launch_aligned(const KParams& p, const Ops& ops, int d, int variant,
                 if (variant == 0) { launch_one<Ops, 32, 4, 2, 4, EXACT, false>(p, ops, s); return true; }
                 if (variant == 2) { launch_one<Ops, 8, 4, 8, 1, EXACT, false>(p, ops, s); return true; }
                 if (variant == 6) { launch_one<Ops, 16, 4, 4, 2, EXACT, false, 2>(p, ops, s); return true; }
-                if (variant == 7) { launch_one<Ops, 16, 4, 4, 4, EXACT, false>(p, ops, s); return true; }
+                if (variant == 7) { launch_one<Ops, 16, 4, 4, 2, EXACT, false>(p, ops, s); return true; }
+                if (variant == 1) { launch_one<Ops, 8, 4, 8, 2, EXACT, false>(p, ops, s); return true; }
+                if (variant == 5) { launch_one<Ops, 32, 4, 2, 8, EXACT, false>(p, ops, s); return true; }
+                launch_one<Ops, 16, 4, 4, 4, EXACT, false>(p, ops, s); return true;  // config 5
             }
             launch_one<Ops, 16, 4, 4, 2, EXACT, false>(p, ops, s); return true;
         case 512: launch_one<Ops, 32, 4, 4, 2, EXACT, false>(p, ops, s); return true;
