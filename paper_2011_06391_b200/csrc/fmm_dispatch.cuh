@@ -7,7 +7,7 @@
 
 namespace fmm {
 
-template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED, int MINB = 0>
+template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED, int MINB = 0, int PF = -1>
 inline void launch_one(const KParams& p, const Ops& ops, cudaStream_t stream) {
     constexpr int kThreads = 256;
     constexpr int GPW = 32 / LPG;
@@ -15,7 +15,7 @@ inline void launch_one(const KParams& p, const Ops& ops, cudaStream_t stream) {
     const int64_t warps = wide + (p.n_narrow_rows + GPW - 1) / GPW;
     if (warps <= 0) return;
     const int64_t blocks = (warps + (kThreads / 32) - 1) / (kThreads / 32);
-    fmm_rows_kernel<Ops, LPG, VEC, NV, UNROLL, EXACT, MASKED, MINB>
+    fmm_rows_kernel<Ops, LPG, VEC, NV, UNROLL, EXACT, MASKED, MINB, PF>
         <<<static_cast<unsigned>(blocks), kThreads, 0, stream>>>(p, ops);
 }
 
@@ -43,7 +43,12 @@ inline bool launch_aligned(const KParams& p, const Ops& ops, int d, int variant,
                 if (variant == 5) { launch_one<Ops, 2, 4, 4, 2, EXACT, false>(p, ops, s); return true; }
                 if (variant == 1) { launch_one<Ops, 4, 4, 2, 4, EXACT, false>(p, ops, s); return true; }
                 if (variant == 7) { launch_one<Ops, 4, 4, 2, 8, EXACT, false, 3>(p, ops, s); return true; }
-                launch_one<Ops, 4, 4, 2, 4, EXACT, false, 4>(p, ops, s); return true;  // config 3
+                if (variant == 8) { launch_one<Ops, 4, 4, 2, 4, EXACT, false, 4, 1>(p, ops, s); return true; }
+                if (variant == 9) { launch_one<Ops, 4, 4, 2, 4, EXACT, false, 4>(p, ops, s); return true; }
+                if (variant == 10) { launch_one<Ops, 4, 4, 2, 4, EXACT, false, 0, 1>(p, ops, s); return true; }
+                if (variant == 11) { launch_one<Ops, 8, 4, 1, 8, EXACT, false, 4, 1>(p, ops, s); return true; }
+                // config 3: 3 blocks/SM with the column prefetch
+                launch_one<Ops, 4, 4, 2, 4, EXACT, false, 3, 1>(p, ops, s); return true;
             }
             launch_one<Ops, 4, 4, 2, 4, EXACT, false>(p, ops, s); return true;
         case 64:

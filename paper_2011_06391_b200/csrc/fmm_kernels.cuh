@@ -435,7 +435,7 @@ __device__ __forceinline__ void gather_rows(const float* __restrict__ Y, int d, 
 // Lane layout: element j = (i*LPG + lane_in_group)*VEC + c.
 // MINB = 0 leaves the register budget to ptxas (as __launch_bounds__(256));
 // MINB > 0 asks for that many resident blocks per SM (tuning variants).
-template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED, int MINB = 0>
+template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED, int MINB = 0, int PF = -1>
 __global__ void __launch_bounds__(256, MINB)
 fmm_rows_kernel(const KParams p, const Ops ops) {
     constexpr int NE = NV * VEC;
@@ -445,7 +445,8 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
     // Fetch column indices one batch ahead on the wide-row fast shapes
     // (config 2: -5%, config 5: -1.5%); for short rows / small d the extra
     // registers cost more than the hidden index latency (measured).
-    constexpr bool kPrefetchCols = !EXACT && !MASKED && (LPG * VEC * NV >= 128);
+    // PF: -1 = this rule, 0 / 1 = forced (tuning variants)
+    constexpr bool kPrefetchCols = PF >= 0 ? (PF == 1) : (!EXACT && !MASKED && (LPG * VEC * NV >= 128));
 
     const int lane = threadIdx.x & 31;
     const int gl = lane & (LPG - 1);
