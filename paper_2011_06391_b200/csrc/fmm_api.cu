@@ -84,6 +84,7 @@ struct GShard {
     int32_t* col = nullptr;
     float* val = nullptr;
     int32_t* order = nullptr;
+    int4* items = nullptr;
     int4* chunks = nullptr;
     int4* split_rows = nullptr;
 };
@@ -181,6 +182,20 @@ bool default_exact(int pattern, int64_t d) {
     return false;
 }
 
+// 1/k when k is a power of two whose reciprocal is a normal float (then
+// s * (1/k) rounds exactly like s / k: both round the same exact value), else 0.
+float exact_reciprocal(float k) {
+    uint32_t b;
+    std::memcpy(&b, &k, sizeof(b));
+    const uint32_t ex = (b >> 23) & 0xffu;
+    if ((b & 0x7fffffu) != 0 || ex == 0 || ex == 0xffu) return 0.0f;  // not a normal power of two
+    const float inv = 1.0f / k;
+    uint32_t bi;
+    std::memcpy(&bi, &inv, sizeof(bi));
+    const uint32_t exi = (bi >> 23) & 0xffu;
+    return (exi == 0 || exi == 0xffu) ? 0.0f : inv;
+}
+
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
 bool launch_rows(const fmm::KParams& p, int pattern, int d, bool exact, bool a16, bool a8,
@@ -253,6 +268,7 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
     p.vop = spec.vop; p.rop = spec.rop; p.sop = spec.sop; p.mop = spec.mop; p.aop = spec.aop;
     p.alpha = spec.alpha;
     p.k = spec.k;
+    p.kinv = exact_reciprocal(spec.k);
     p.mlp_wx = spec.mlp_wx;
     p.mlp_wy = spec.mlp_wy;
     p.mlp_b = spec.mlp_b;
@@ -263,6 +279,7 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
         p.chunks = gs.chunks;
         p.n_chunk_items = gs.n_chunks;
         p.order = gs.order + gs.n_split_rows;
+        p.items = gs.items + gs.n_split_rows;
         p.n_wide_rows = gs.n_wide_rows;
         p.n_narrow_rows = rows - gs.n_split_rows - gs.n_wide_rows;
     } else {
@@ -270,6 +287,7 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
         p.chunks = nullptr;
         p.n_chunk_items = 0;
         p.order = gs.order;
+        p.items = gs.items;
         p.n_wide_rows = 0;
         p.n_narrow_rows = rows;
     }
@@ -654,8 +672,10 @@ fmm_status fmm_graph_upload(fmm_ctx* ctx, int64_t m, int64_t n, const int64_t* r
         if ((st = upload_vec(ctx, P.local_row_ptr, &gs.row_ptr)) != FMM_OK) break;
         if ((st = upload_vec(ctx, P.order, &gs.order)) != FMM_OK) break;
         static_assert(sizeof(fmm::Int4) == sizeof(int4), "int4 layout");
-        std::vector<int4> ch(P.chunks.size()), sr(P.split_rows.size());
+        std::vector<int4> ch(P.chunks.size()), sr(P.split_rows.size()), it(P.items.size());
         std::memcpy(ch.data(), P.chunks.data(), ch.size() * sizeof(int4));
+        std::memcpy(it.data(), P.items.data(), it.size() * sizeof(int4));
+        if ((st = upload_vec(ctx, it, &gs.items)) != FMM_OK) break;
         std::memcpy(sr.data(), P.split_rows.data(), sr.size() * sizeof(int4));
         if ((st = upload_vec(ctx, ch, &gs.chunks)) != FMM_OK) break;
         if ((st = upload_vec(ctx, sr, &gs.split_rows)) != FMM_OK) break;
@@ -711,7 +731,7 @@ fmm_status fmm_graph_free(fmm_graph* g) {
                             static_cast<void*>(sd.warp_steps), static_cast<void*>(sd.empty_rows)})
                 if (q) cudaFree(q);
         for (void* p : {static_cast<void*>(gs.row_ptr), static_cast<void*>(gs.col), static_cast<void*>(gs.val),
-                        static_cast<void*>(gs.order), static_cast<void*>(gs.chunks),
+                        static_cast<void*>(gs.order), static_cast<void*>(gs.items), static_cast<void*>(gs.chunks),
                         static_cast<void*>(gs.split_rows)})
             if (p) cudaFree(p);
     }

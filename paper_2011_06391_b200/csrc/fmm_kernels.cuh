@@ -47,6 +47,8 @@ struct KParams {
     float* Z;                // z_r = Z + r * d   (r shard-local)
     float* partial;          // chunk partial rows: partial + slot * d
     const int32_t* order;    // rows, heavy first: wide rows then narrow rows
+    const int4* items;       // per order slot {row, e0 lo, e0 hi, degree}: one
+                             // load replaces order[i] -> row_ptr[r], row_ptr[r+1]
     const int4* chunks;      // chunk items {row, k, slot, 0}
     int64_t n_chunk_items;
     int64_t n_wide_rows;     // rows a whole warp folds (edges over its groups)
@@ -57,6 +59,7 @@ struct KParams {
     // dynamic op codes (used by DOps only)
     int vop, rop, sop, mop, aop;
     float alpha, k;
+    float kinv;  // 1/k when k is a power of two (exact), else 0
     float mlp_wx, mlp_wy, mlp_b;
     // fused exchange: every final z row is also stored to zpeer[q] + r*d —
     // the other shards' next-iterate buffers, reached over NVLink (P2P) — so
@@ -172,7 +175,7 @@ __device__ __forceinline__ float vop_rop_step(const Ops& ops, float acc, float x
 // 1/(1+exp(-s)) with CUDA's accurate expf (no LUT, no clamp);
 // the exact scheme divides with IEEE rounding, the fast one uses recip_ge1.
 template <bool EXACT, class Ops>
-__device__ __forceinline__ float sop_apply(const Ops& ops, float s, float alpha, float k) {
+__device__ __forceinline__ float sop_apply(const Ops& ops, float s, float alpha, float k, float kinv = 0.0f) {
     switch (ops.sop()) {
         case FMM_SOP_SIGMOID: return sigmoid_f<EXACT>(s);
         case FMM_SOP_SCAL: return __fmul_rn(alpha, s);
@@ -180,7 +183,9 @@ __device__ __forceinline__ float sop_apply(const Ops& ops, float s, float alpha,
             // s >= 0 after a squared / plain norm, so 1+s >= 1
             if (!EXACT && (ops.rop() == FMM_ROP_SQNORM || ops.rop() == FMM_ROP_NORM)) return recip_ge1(1.0f + s);
             return 1.0f / (1.0f + s);
-        case FMM_SOP_SQK: return __fdiv_rn(s, k);
+        // s / k; for k a power of two (kinv = 1/k exact and normal) the
+        // product s * kinv is the same correctly rounded value in one FMUL
+        case FMM_SOP_SQK: return kinv != 0.0f ? __fmul_rn(s, kinv) : __fdiv_rn(s, k);
         default: return s;  // NOOP
     }
 }
@@ -302,7 +307,7 @@ __device__ __forceinline__ void consume_edges(const Ops& ops, const KParams& p, 
             for (int u = 0; u < U; ++u) {
                 float sv = s[u];
                 if (ops.rop() == FMM_ROP_NORM) sv = sqrtf(sv);
-                float h = sop_apply<EXACT>(ops, sv, p.alpha, p.k);
+                float h = sop_apply<EXACT>(ops, sv, p.alpha, p.k, p.kinv);
                 h = ok[u] ? h : 0.0f;
                 if (ops.mop() == FMM_MOP_MUL_VOP) h *= a[u];
                 const float2 h2 = make_float2(h, h);
@@ -353,7 +358,7 @@ __device__ __forceinline__ void consume_edges(const Ops& ops, const KParams& p, 
         for (int u = 0; u < U; ++u) {
             float sv = s[u];
             if (ops.rop() == FMM_ROP_NORM) sv = sqrtf(sv);
-            float h = sop_apply<EXACT>(ops, sv, p.alpha, p.k);
+            float h = sop_apply<EXACT>(ops, sv, p.alpha, p.k, p.kinv);
             if (predicated) {
                 h = ok[u] ? h : 0.0f;
             } else if (!ok[u]) {
@@ -389,7 +394,7 @@ __device__ __forceinline__ void consume_edges(const Ops& ops, const KParams& p, 
 #pragma unroll
             for (int e = 0; e < NE; ++e) {
                 float t = vop_apply<EXACT>(ops, x[e], y[u][e]);
-                t = sop_apply<EXACT>(ops, t, p.alpha, p.k);
+                t = sop_apply<EXACT>(ops, t, p.alpha, p.k, p.kinv);
                 float w;
                 if (ops.mop() == FMM_MOP_SEL2ND) {
                     w = y[u][e];
@@ -468,9 +473,10 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
             e1 = min(e0 + static_cast<int64_t>(p.chunk), p.row_ptr[r + 1]);
             out = p.partial + static_cast<int64_t>(c.z) * (MASKED ? p.d : LPG * VEC * NV);
         } else {
-            r = p.order[warp - p.n_chunk_items];
-            e0 = p.row_ptr[r];
-            e1 = p.row_ptr[r + 1];
+            const int4 it = __ldg(p.items + (warp - p.n_chunk_items));
+            r = it.x;
+            e0 = static_cast<int64_t>(static_cast<uint32_t>(it.y)) | (static_cast<int64_t>(it.z) << 32);
+            e1 = e0 + it.w;
             out = p.Z + r * (MASKED ? p.d : LPG * VEC * NV);
         }
     } else {
@@ -478,9 +484,10 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
         active = idx < p.n_narrow_rows;
         if (__all_sync(0xffffffffu, !active)) return;
         if (active) {
-            r = p.order[p.n_wide_rows + idx];
-            e0 = p.row_ptr[r];
-            e1 = p.row_ptr[r + 1];
+            const int4 it = __ldg(p.items + (p.n_wide_rows + idx));
+            r = it.x;
+            e0 = static_cast<int64_t>(static_cast<uint32_t>(it.y)) | (static_cast<int64_t>(it.z) << 32);
+            e1 = e0 + it.w;
             out = p.Z + r * (MASKED ? p.d : LPG * VEC * NV);
         }
     }

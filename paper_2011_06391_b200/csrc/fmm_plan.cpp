@@ -84,6 +84,15 @@ ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t ro
     for (int k = 0; k < kKeys; ++k) count[k + 1] += count[k];
     P.order.resize(static_cast<size_t>(rows));
     for (int64_t r = 0; r < rows; ++r) P.order[count[key_of(r)]++] = static_cast<int32_t>(r);
+    P.items.resize(static_cast<size_t>(rows));
+    for (int64_t i = 0; i < rows; ++i) {
+        const int32_t r = P.order[i];
+        const int64_t e0 = P.local_row_ptr[r];
+        const int64_t deg = P.local_row_ptr[r + 1] - e0;
+        if (deg > INT32_MAX) throw std::invalid_argument("row degree >= 2^31");
+        P.items[i] = {r, static_cast<int32_t>(static_cast<uint32_t>(e0 & 0xffffffffll)),
+                      static_cast<int32_t>(e0 >> 32), static_cast<int32_t>(deg)};
+    }
 
     // chunk items for the split prefix, slots assigned row by row
     int64_t slot = 0;

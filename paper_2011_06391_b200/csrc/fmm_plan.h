@@ -42,6 +42,10 @@ struct ShardPlan {
     // descending power-of-two degree bucket, stable (natural order) inside a
     // bucket so light rows keep their memory locality.
     std::vector<int32_t> order;
+    // items[i] = {order[i], e0 low 32 bits, e0 high 32 bits, degree} with e0
+    // the row's first local edge: the kernels read a row's whole descriptor
+    // with one 16-byte load
+    std::vector<Int4> items;
     int64_t n_split_rows = 0;             // prefix of `order` cut into chunks
     int64_t n_wide_rows = 0;              // next rows with degree >= kWideMin
     std::vector<Int4> chunks;             // {row, k, slot, 0}

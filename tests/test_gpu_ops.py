@@ -207,3 +207,16 @@ def test_cpp_wrapper_runs(tmp_path):
     assert r.returncode == 0, r.stderr
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "wrapper ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("k", [1.0, 0.25, 4.0, -2.0, 2.0 ** -120, 2.0 ** 120, 3.0, 0.1])
+def test_sqk_division_bit_exact_for_every_k(k):
+    """SOP_SQK divides by k; for k a power of two the kernels multiply by the
+    exact reciprocal instead (the same correctly rounded value). Bit-exact
+    against the reference order on the exact scheme for powers of two,
+    extreme exponents (reciprocal near the normal range limits) and
+    non-powers (IEEE division kept)."""
+    A, X, Y = random_case(int(abs(np.log2(abs(k)))) + 5, 50, 50, 2, weighted=False, lo=-3.0, hi=3.0)
+    spec = F.fr_attract_spec(k)
+    Z = F.fused_mm(A, X, Y, spec, 1, opts=F.KernelOptions(exact=True))
+    check_exact(Z.array, oracle.oracle_fused_mm(A, X, Y, spec))
