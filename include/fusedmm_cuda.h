@@ -204,6 +204,30 @@ fmm_status fmm_iterate(fmm_ctx* ctx, const fmm_graph* g,
                        const fmm_opspec* spec, int64_t d, float* X, int iters,
                        uint32_t flags, fmm_stats* stats);
 
+/* ---- device-side graph construction ----------- */
+
+/* csr_from_coo on GPU `device` (replaces fusedmm::csr_from_coo,
+ * matrix.hpp:87-140): entries (rows[i], cols[i], vals[i]) in insertion
+ * order; duplicates summed left to right into the first occurrence; per-row
+ * storage order is first-occurrence order. vals NULL means every value is 1.
+ * Host arrays: row_ptr[m+1]; col_idx / values (NULL to skip) with room for
+ * `count` entries; *nnz_out = entries written. FMM_E_INVAL for an entry out of
+ * bounds (the reference throws std::invalid_argument). Applied to the R-MAT
+ * insertion stream this is rmat_generate (rmat.hpp:24-61). */
+fmm_status fmm_csr_from_coo(int device, int64_t m, int64_t n, int64_t count,
+                            const int64_t* rows, const int64_t* cols,
+                            const float* vals, int64_t* row_ptr,
+                            int64_t* col_idx, float* values, int64_t* nnz_out);
+
+/* The BASELINE.json graph recipe on GPU `device`: an n x n edge list with
+ * self-loops dropped (drop_self), both directions added (symmetrize), sorted
+ * and deduplicated; unweighted (a_uv = 1). Host arrays: row_ptr[n+1], col_idx
+ * with room for 2*count entries. */
+fmm_status fmm_csr_sym_unique(int device, int64_t n, int64_t count,
+                              const int64_t* rows, const int64_t* cols,
+                              int drop_self, int symmetrize, int64_t* row_ptr,
+                              int64_t* col_idx, int64_t* nnz_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -241,5 +241,35 @@ Dense fused_mm(const Csr& A, const Dense& X, const Dense& Y, const fmm_opspec& o
     return detail::run(A, X, Y, ops, t, stats);
 }
 
+// csr_from_coo on the GPU (matrix.hpp:87-140): same signature shape as the
+// reference (entries with .row/.col/.value, m, n), same result, same
+// std::invalid_argument for an out-of-bounds entry. Csr is the caller's CSR
+// type (the reference's CsrMatrix<float> or types::CsrMatrix).
+template <class Csr, class Entry>
+Csr csr_from_coo(const std::vector<Entry>& entries, int64_t m, int64_t n, int device = 0) {
+    const size_t cnt = entries.size();
+    std::vector<int64_t> rows(cnt), cols(cnt);
+    std::vector<float> vals(cnt);
+    for (size_t i = 0; i < cnt; ++i) {
+        rows[i] = entries[i].row;
+        cols[i] = entries[i].col;
+        vals[i] = static_cast<float>(entries[i].value);
+    }
+    Csr A;
+    A.nrows = m;
+    A.ncols = n;
+    A.row_ptr.assign(static_cast<size_t>(m) + 1, 0);
+    A.col_idx.assign(cnt, 0);
+    A.values.assign(cnt, 0.f);
+    int64_t nnz = 0;
+    const fmm_status st = fmm_csr_from_coo(device, m, n, static_cast<int64_t>(cnt), rows.data(), cols.data(),
+                                           vals.data(), A.row_ptr.data(), A.col_idx.data(), A.values.data(), &nnz);
+    if (st == FMM_E_INVAL) throw std::invalid_argument("csr_from_coo: entry out of bounds");
+    throw_status(st);
+    A.col_idx.resize(static_cast<size_t>(nnz));
+    A.values.resize(static_cast<size_t>(nnz));
+    return A;
+}
+
 }  // namespace cuda
 }  // namespace fusedmm

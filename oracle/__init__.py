@@ -88,6 +88,8 @@ def ref_lib() -> C.CDLL:
         L.fmm_ref_rmat.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_uint64,
                                    P64, P64, PF]
         L.fmm_ref_pattern_of.argtypes = [C.POINTER(or_spec)]
+        L.fmm_ref_csr_from_coo.restype = C.c_int64
+        L.fmm_ref_csr_from_coo.argtypes = [C.c_int64, C.c_int64, C.c_int64, P64, P64, PF, P64, P64, PF]
         _ref = L
     return _ref
 
@@ -215,6 +217,57 @@ def ref_rmat(scale: int, edge_factor: int, seed: int, abc=(0.57, 0.19, 0.19)):
     L.fmm_ref_rmat(scale, edge_factor, *abc, seed, rp.ctypes.data_as(P64), cl.ctypes.data_as(P64),
                    vl.ctypes.data_as(PF))
     return rp, cl, vl
+
+
+def ref_csr_from_coo(rows, cols, vals, m: int, n: int):
+    """The unmodified reference csr_from_coo (matrix.hpp:87-140) as
+    (row_ptr, col, val); raises ValueError where the reference throws."""
+    rows = np.ascontiguousarray(rows, np.int64)
+    cols = np.ascontiguousarray(cols, np.int64)
+    cnt = rows.size
+    v = None if vals is None else np.ascontiguousarray(vals, np.float32)
+    rp = np.zeros(m + 1, np.int64)
+    cl = np.zeros(max(cnt, 1), np.int64)
+    vl = np.zeros(max(cnt, 1), np.float32)
+    nnz = ref_lib().fmm_ref_csr_from_coo(m, n, cnt, rows.ctypes.data_as(P64), cols.ctypes.data_as(P64),
+                                         None if v is None else v.ctypes.data_as(PF), rp.ctypes.data_as(P64),
+                                         cl.ctypes.data_as(P64), vl.ctypes.data_as(PF))
+    if nnz < 0:
+        raise ValueError("csr_from_coo: entry out of bounds")
+    return rp, cl[:nnz], vl[:nnz]
+
+
+def oracle_csr_from_coo(rows, cols, vals, m: int, n: int):
+    """CPU restatement of csr_from_coo (matrix.hpp:87-140), test
+    infrastructure: bounds check (matrix.hpp:89-95); counting placement of the
+    entries by row in insertion order (matrix.hpp:97-111); per row, the first
+    occurrence of a column keeps its slot and later duplicates are added to it
+    in insertion order with float32 arithmetic (matrix.hpp:120-131)."""
+    rows = np.asarray(rows, np.int64)
+    cols = np.asarray(cols, np.int64)
+    vals = np.ones(rows.size, np.float32) if vals is None else np.asarray(vals, np.float32)
+    if rows.size and (rows.min() < 0 or rows.max() >= m or cols.min() < 0 or cols.max() >= n):
+        raise ValueError("csr_from_coo: entry out of bounds")
+    order = np.argsort(rows, kind="stable")  # counting placement == stable by row
+    row_ptr = np.zeros(m + 1, np.int64)
+    out_c: list = []
+    out_v: list = []
+    start = 0
+    sr = rows[order]
+    bounds = np.searchsorted(sr, np.arange(m + 1), side="left")
+    for r in range(m):
+        seen: dict = {}
+        for p in order[bounds[r]:bounds[r + 1]]:
+            c = int(cols[p])
+            if c in seen:
+                out_v[seen[c]] = np.float32(out_v[seen[c]] + vals[p])
+            else:
+                seen[c] = len(out_c)
+                out_c.append(c)
+                out_v.append(np.float32(vals[p]))
+        row_ptr[r + 1] = len(out_c)
+        start = len(out_c)
+    return row_ptr, np.array(out_c, np.int64), np.array(out_v, np.float32)
 
 
 def row_errors(Z_gpu: np.ndarray, Z_cpu: np.ndarray) -> np.ndarray:

@@ -207,6 +207,23 @@ int64_t fmm_ref_rmat(int scale, int edge_factor, double a, double b, double c, u
     return A.nnz();
 }
 
+// csr_from_coo (matrix.hpp:87-140) over flat arrays; returns nnz or -1 when
+// the reference throws (entry out of bounds). Outputs sized for `count`.
+int64_t fmm_ref_csr_from_coo(int64_t m, int64_t n, int64_t count, const int64_t* rows, const int64_t* cols,
+                             const float* vals, int64_t* row_ptr, int64_t* col, float* val) {
+    std::vector<CooEntry<float>> ent(static_cast<size_t>(count));
+    for (int64_t i = 0; i < count; ++i) ent[i] = {rows[i], cols[i], vals ? vals[i] : 1.0f};
+    try {
+        auto A = csr_from_coo<float>(ent, m, n);
+        std::memcpy(row_ptr, A.row_ptr.data(), sizeof(int64_t) * A.row_ptr.size());
+        std::memcpy(col, A.col_idx.data(), sizeof(int64_t) * A.col_idx.size());
+        std::memcpy(val, A.values.data(), sizeof(float) * A.values.size());
+        return A.nnz();
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
 int fmm_ref_pattern_of(const RefSpec* s) {
     return static_cast<int>(pattern_of(make_ref_spec<float>(*s)));
 }

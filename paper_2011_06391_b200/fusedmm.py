@@ -274,6 +274,47 @@ def csr_from_coo(entries: Sequence[tuple], m: int, n: int) -> CsrMatrix:
                      np.array(vals, dtype=np.float32))
 
 
+def csr_from_coo_device(rows, cols, vals, m: int, n: int, device: int = 0) -> CsrMatrix:
+    """csr_from_coo (matrix.hpp:87-140) built on the GPU (fmm_csr_from_coo):
+    flat arrays in insertion order; vals None means all ones. Same result and
+    same InvalidArgument as the reference for an out-of-bounds entry."""
+    rows = np.ascontiguousarray(rows, np.int64)
+    cols = np.ascontiguousarray(cols, np.int64)
+    cnt = int(rows.size)
+    if cols.size != cnt:
+        raise InvalidArgument("csr_from_coo: rows and cols differ in length")
+    v = None if vals is None else np.ascontiguousarray(vals, np.float32)
+    rp = np.zeros(m + 1, np.int64)
+    cl = np.zeros(max(cnt, 1), np.int64)
+    vl = np.zeros(max(cnt, 1), np.float32)
+    nnz = C.c_int64()
+    st = _lib.lib().fmm_csr_from_coo(device, m, n, cnt, _i64(rows), _i64(cols),
+                                     None if v is None else _f32(v), _i64(rp), _i64(cl), _f32(vl), C.byref(nnz))
+    if st == _lib.FMM_E_INVAL:
+        raise InvalidArgument(f"csr_from_coo: entry out of bounds for {m}x{n}")
+    _raise(st)
+    k = nnz.value
+    return CsrMatrix(m, n, rp, cl[:k].copy(), vl[:k].copy())
+
+
+def csr_sym_unique_device(rows, cols, n: int, drop_self: bool = True, symmetrize: bool = True,
+                          device: int = 0) -> CsrMatrix:
+    """The BASELINE.json graph recipe on the GPU (fmm_csr_sym_unique): drop
+    self-loops, add both directions, sort, deduplicate; unweighted."""
+    rows = np.ascontiguousarray(rows, np.int64)
+    cols = np.ascontiguousarray(cols, np.int64)
+    cnt = int(rows.size)
+    rp = np.zeros(n + 1, np.int64)
+    cl = np.zeros(max(2 * cnt, 1), np.int64)
+    nnz = C.c_int64()
+    st = _lib.lib().fmm_csr_sym_unique(device, n, cnt, _i64(rows), _i64(cols), int(drop_self), int(symmetrize),
+                                       _i64(rp), _i64(cl), C.byref(nnz))
+    if st == _lib.FMM_E_INVAL:
+        raise InvalidArgument("csr_sym_unique: vertex out of range")
+    _raise(st)
+    return CsrMatrix(n, n, rp, cl[:nnz.value].copy(), None)
+
+
 def validate(A: CsrMatrix) -> Optional[str]:
     """matrix.hpp:143-166: first CSR invariant violation, or None."""
     if A.row_ptr.size != A.nrows + 1:

@@ -65,6 +65,17 @@ int main() {
     Ye.data = {3, 4};
     DenseMatrix Ze = fc::fused_mm(E, Xe, Ye, fc::tdist_ops(), 1);
     CHECK(std::fabs(Ze.data[0] + 2.f / 9.f) < 1e-6f);
+    // csr_from_coo on the device: duplicates summed into the first
+    // occurrence, first-occurrence order (matrix.hpp:87-140)
+    struct Coo { int64_t row, col; float value; };
+    std::vector<Coo> ent = {{1, 2, 1.f}, {0, 1, 2.f}, {1, 0, 3.f}, {1, 2, 4.f}, {0, 1, 0.5f}};
+    CsrMatrix Cc = fc::csr_from_coo<CsrMatrix>(ent, 2, 3);
+    CHECK(Cc.row_ptr == (std::vector<int64_t>{0, 1, 3}));
+    CHECK(Cc.col_idx == (std::vector<int64_t>{1, 2, 0}));
+    CHECK(Cc.values == (std::vector<float>{2.5f, 5.f, 3.f}));
+    threw = false;
+    try { fc::csr_from_coo<CsrMatrix>(std::vector<Coo>{{2, 0, 1.f}}, 2, 3); } catch (const std::invalid_argument&) { threw = true; }
+    CHECK(threw);
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "wrapper ok", failures);
     return failures ? 1 : 0;
 }
