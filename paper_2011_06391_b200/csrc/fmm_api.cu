@@ -198,16 +198,16 @@ float exact_reciprocal(float k) {
 
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
-bool launch_rows(const fmm::KParams& p, int pattern, int d, bool exact, bool a16, bool a8,
+bool launch_rows(const fmm::KParams& p, int pattern, int d, bool exact, bool a32, bool a16, bool a8,
                  int variant, cudaStream_t s) {
     const bool vec = fmm::aligned_shape(d, a16, a8);
     if (vec) {
         switch (pattern) {
-            case FMM_PATTERN_SIGMOID_EMBED: return fmm::launch_sigmoid(p, d, exact, variant, s);
-            case FMM_PATTERN_SPMM_GCN: return fmm::launch_gcn(p, d, exact, variant, s);
-            case FMM_PATTERN_FR_LAYOUT: return fmm::launch_fr(p, d, exact, variant, s);
-            case FMM_PATTERN_TDIST: return fmm::launch_tdist(p, d, exact, variant, s);
-            case FMM_PATTERN_FR_ATTRACT: return fmm::launch_frattr(p, d, exact, variant, s);
+            case FMM_PATTERN_SIGMOID_EMBED: return fmm::launch_sigmoid(p, d, exact, variant, a32, s);
+            case FMM_PATTERN_SPMM_GCN: return fmm::launch_gcn(p, d, exact, variant, a32, s);
+            case FMM_PATTERN_FR_LAYOUT: return fmm::launch_fr(p, d, exact, variant, a32, s);
+            case FMM_PATTERN_TDIST: return fmm::launch_tdist(p, d, exact, variant, a32, s);
+            case FMM_PATTERN_FR_ATTRACT: return fmm::launch_frattr(p, d, exact, variant, a32, s);
             default: break;
         }
     }
@@ -297,6 +297,9 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
                      (partial == nullptr || aligned(partial, 16)) && (a % 16 == 0);
     const bool a8 = (d % 2 == 0) && aligned(X, 8) && aligned(Y, 8) && aligned(Z, 8) &&
                     (partial == nullptr || aligned(partial, 8));
+    bool a32 = (d % 8 == 0) && aligned(X, 32) && aligned(Y, 32) && aligned(Z, 32) &&
+               (partial == nullptr || aligned(partial, 32));
+    for (int q = 0; q < po.n; ++q) a32 = a32 && aligned(po.p[q], 32);
     // fast scheme, hot patterns: the persistent cp.async-pipelined kernel
     int gpw = 0, su = 0;
     const bool sched_pattern = pattern == FMM_PATTERN_SIGMOID_EMBED || pattern == FMM_PATTERN_TDIST ||
@@ -342,7 +345,7 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
         }
     }
     if (variant < -1) variant = -1;
-    if (!launch_rows(p, pattern, static_cast<int>(d), exact, a16, a8, variant, stream)) return -1;
+    if (!launch_rows(p, pattern, static_cast<int>(d), exact, a32, a16, a8, variant, stream)) return -1;
     int launches = 1;
     if (split && gs.n_split_rows > 0) {
         fmm::fmm_combine_kernel<<<static_cast<unsigned>(gs.n_split_rows), 256, 0, stream>>>(

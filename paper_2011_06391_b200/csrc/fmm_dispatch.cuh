@@ -21,6 +21,42 @@ inline void launch_one(const KParams& p, const Ops& ops, cudaStream_t stream) {
 
 // Vectorised shapes: d = LPG * VEC * NV exactly, rows VEC*4-byte aligned.
 // variant < 0 selects the default shape for d; others exist for tuning.
+// 256-bit shapes (VEC = 8; rows 32-byte aligned, d % 8 == 0): twice the bytes
+// per gather request of the VEC = 4 shapes. variant 20 selects the VEC = 4
+// default instead, 21-23 are tuning alternatives.
+template <class Ops, bool EXACT>
+inline bool launch_aligned32(const KParams& p, const Ops& ops, int d, int variant, cudaStream_t s) {
+    switch (d) {
+        case 32:
+            if constexpr (!EXACT) {
+                if (variant == 21) { launch_one<Ops, 2, 8, 2, 4, EXACT, false, 3, 1>(p, ops, s); return true; }
+                if (variant == 22) { launch_one<Ops, 4, 8, 1, 8, EXACT, false, 3, 1>(p, ops, s); return true; }
+                if (variant == 23) { launch_one<Ops, 4, 8, 1, 4, EXACT, false, 4, 1>(p, ops, s); return true; }
+                launch_one<Ops, 4, 8, 1, 4, EXACT, false, 3, 1>(p, ops, s); return true;  // config 3
+            }
+            launch_one<Ops, 4, 8, 1, 4, EXACT, false>(p, ops, s); return true;
+        case 64:
+            launch_one<Ops, 8, 8, 1, 4, EXACT, false>(p, ops, s); return true;  // config 1
+        case 128:
+            if constexpr (!EXACT) {
+                if (variant == 21) { launch_one<Ops, 4, 8, 4, 4, EXACT, false>(p, ops, s); return true; }
+                if (variant == 22) { launch_one<Ops, 16, 8, 1, 4, EXACT, false>(p, ops, s); return true; }
+                if (variant == 23) { launch_one<Ops, 8, 8, 2, 2, EXACT, false>(p, ops, s); return true; }
+                launch_one<Ops, 8, 8, 2, 4, EXACT, false>(p, ops, s); return true;  // config 2
+            }
+            launch_one<Ops, 8, 8, 2, 2, EXACT, false>(p, ops, s); return true;
+        case 256:
+            if constexpr (!EXACT) {
+                if (variant == 21) { launch_one<Ops, 32, 8, 1, 4, EXACT, false>(p, ops, s); return true; }
+                if (variant == 22) { launch_one<Ops, 8, 8, 4, 2, EXACT, false>(p, ops, s); return true; }
+                if (variant == 23) { launch_one<Ops, 16, 8, 2, 2, EXACT, false>(p, ops, s); return true; }
+                launch_one<Ops, 16, 8, 2, 4, EXACT, false>(p, ops, s); return true;  // config 5
+            }
+            launch_one<Ops, 16, 8, 2, 2, EXACT, false>(p, ops, s); return true;
+        default: return false;
+    }
+}
+
 template <class Ops, bool EXACT>
 inline bool launch_aligned(const KParams& p, const Ops& ops, int d, int variant, cudaStream_t s) {
     switch (d) {
@@ -109,19 +145,24 @@ inline bool aligned_shape(int d, bool aligned16, bool aligned8) {
     }
 }
 
-bool launch_sigmoid(const KParams& p, int d, bool exact, int variant, cudaStream_t s);
-bool launch_gcn(const KParams& p, int d, bool exact, int variant, cudaStream_t s);
-bool launch_fr(const KParams& p, int d, bool exact, int variant, cudaStream_t s);
-bool launch_tdist(const KParams& p, int d, bool exact, int variant, cudaStream_t s);
-bool launch_frattr(const KParams& p, int d, bool exact, int variant, cudaStream_t s);
+bool launch_sigmoid(const KParams& p, int d, bool exact, int variant, bool a32, cudaStream_t s);
+bool launch_gcn(const KParams& p, int d, bool exact, int variant, bool a32, cudaStream_t s);
+bool launch_fr(const KParams& p, int d, bool exact, int variant, bool a32, cudaStream_t s);
+bool launch_tdist(const KParams& p, int d, bool exact, int variant, bool a32, cudaStream_t s);
+bool launch_frattr(const KParams& p, int d, bool exact, int variant, bool a32, cudaStream_t s);
 bool launch_generic(const KParams& p, int d, bool exact, bool vectorised, cudaStream_t s);
 
 }  // namespace fmm
 
 #define FMM_DEFINE_STATIC_LAUNCH(NAME, OPS)                                        \
     namespace fmm {                                                                \
-    bool NAME(const KParams& p, int d, bool exact, int variant, cudaStream_t s) {  \
+    bool NAME(const KParams& p, int d, bool exact, int variant, bool a32, cudaStream_t s) { \
         const OPS ops{};                                                           \
+        if (a32 && variant != 20 && (variant < 0 || variant > 20) &&              \
+            (exact ? launch_aligned32<OPS, true>(p, ops, d, variant, s)           \
+                   : launch_aligned32<OPS, false>(p, ops, d, variant, s)))        \
+            return true;                                                           \
+        if (variant == 20) variant = -1;                                           \
         return exact ? launch_aligned<OPS, true>(p, ops, d, variant, s)            \
                      : launch_aligned<OPS, false>(p, ops, d, variant, s);          \
     }                                                                              \

@@ -203,14 +203,26 @@ __device__ __forceinline__ float aop_identity(const Ops& ops) {
 }
 
 // ------------------------------------------------------------ memory ops
+// 32-byte vector (sm_100a 256-bit LDG/STG: LDG.E.ENL2.256). Random row
+// gathers served from L2 deliver ~1.7x more bytes per SM with 256-bit than
+// with 128-bit requests (profiles/r03_probe_ldg256.log: 19.0 vs 11.2 TB/s).
+struct alignas(32) float8v {
+    float v[8];
+};
 template <int VEC> struct VecT;
+template <> struct VecT<8> { using T = float8v; };
 template <> struct VecT<4> { using T = float4; };
 template <> struct VecT<2> { using T = float2; };
 template <> struct VecT<1> { using T = float; };
 
 template <int VEC>
 __device__ __forceinline__ void load_vec(float* dst, const float* src) {
-    if constexpr (VEC == 4) {
+    if constexpr (VEC == 8) {
+        asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(dst[0]), "=f"(dst[1]), "=f"(dst[2]), "=f"(dst[3]), "=f"(dst[4]), "=f"(dst[5]),
+                       "=f"(dst[6]), "=f"(dst[7])
+                     : "l"(src));
+    } else if constexpr (VEC == 4) {
         float4 v = __ldg(reinterpret_cast<const float4*>(src));
         dst[0] = v.x; dst[1] = v.y; dst[2] = v.z; dst[3] = v.w;
     } else if constexpr (VEC == 2) {
@@ -222,7 +234,11 @@ __device__ __forceinline__ void load_vec(float* dst, const float* src) {
 }
 template <int VEC>
 __device__ __forceinline__ void store_vec(float* dst, const float* src) {
-    if constexpr (VEC == 4) {
+    if constexpr (VEC == 8) {
+        asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "f"(src[0]), "f"(src[1]),
+                     "f"(src[2]), "f"(src[3]), "f"(src[4]), "f"(src[5]), "f"(src[6]), "f"(src[7])
+                     : "memory");
+    } else if constexpr (VEC == 4) {
         *reinterpret_cast<float4*>(dst) = make_float4(src[0], src[1], src[2], src[3]);
     } else if constexpr (VEC == 2) {
         *reinterpret_cast<float2*>(dst) = make_float2(src[0], src[1]);

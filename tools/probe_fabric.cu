@@ -30,6 +30,7 @@ namespace cg = cooperative_groups;
 // MODE 1: all gathers from the cluster's smem (rank idx % csize, slot (idx / csize) % H), ld.shared::cluster
 // MODE 2: idx < split -> cluster smem, else global
 // MODE 3: all gathers from the CTA's own smem (slot idx % H), ld.shared
+// MODE 4: idx < split -> own smem, else global
 // H is a power of two, csize a power of two.
 __device__ __forceinline__ float4 ld_nc4(const float4* p) {
     float4 v;
@@ -90,9 +91,9 @@ __global__ void __launch_bounds__(512, 1) gather_kernel(const float4* __restrict
         float4 val[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if (MODE == 0 || (MODE == 2 && v[u] >= split)) {
+            if (MODE == 0 || ((MODE == 2 || MODE == 4) && v[u] >= split)) {
                 val[u] = ld_nc4(Y + (int64_t)v[u] * ROW + gl);
-            } else if (MODE == 3) {
+            } else if (MODE == 3 || MODE == 4) {
                 val[u] = ld_smem4(sbase + (((v[u] & (H - 1)) * ROW + gl) << 4));
             } else {
                 const int r = v[u] & (csize - 1);
@@ -190,6 +191,8 @@ int main() {
             run<8, 8, 0>(Y, idx_hot, n_idx, H, 0, 1, 2, 512, out, nsm);
             run<8, 4, 0>(Y, idx_hot, n_idx, H, 0, 1, 4, 256, out, nsm);
             run<8, 4, 3>(Y, idx_hot, n_idx, H, 0, 1, 1, 512, out, nsm);    // own smem
+            for (int f : {10, 25, 50}) run<8, 4, 4>(Y, idx_hot, n_idx, H, (int)(hot_rows * f / 100), 1, 1, 512, out, nsm);
+            for (int f : {10, 25, 50}) run<8, 4, 4>(Y, idx_cold, n_idx, H, (int)((1ll << 30) / 128 * f / 100), 1, 1, 512, out, nsm);
             for (int cs : {1, 2, 4, 8, 16}) run<8, 4, 1>(Y, idx_hot, n_idx, H, 0, cs, 1, 512, out, nsm);
             run<8, 8, 1>(Y, idx_hot, n_idx, H, 0, 8, 1, 512, out, nsm);
             for (int f : {25, 50}) {
@@ -202,6 +205,7 @@ int main() {
             run<32, 4, 0>(Y, idx_cold, n_idx, H, 0, 1, 2, 512, out, nsm);
             run<32, 4, 0>(Y, idx_hot, n_idx, H, 0, 1, 2, 512, out, nsm);
             run<32, 4, 3>(Y, idx_hot, n_idx, H, 0, 1, 1, 512, out, nsm);
+            for (int f : {10, 25, 50}) run<32, 4, 4>(Y, idx_hot, n_idx, H, (int)(hot_rows * f / 100), 1, 1, 512, out, nsm);
             for (int cs : {1, 2, 4, 8, 16}) run<32, 4, 1>(Y, idx_hot, n_idx, H, 0, cs, 1, 512, out, nsm);
             for (int f : {25, 50}) {
                 const int split = (int)(hot_rows * f / 100);

@@ -76,6 +76,39 @@ __global__ void __launch_bounds__(256) ldg_kernel(const float4* __restrict__ Y, 
     if (acc.x + acc.y + acc.z + acc.w == 12345.f) out[0] = acc.x;
 }
 
+// 256-bit per-lane loads (sm_100a LDG.E.ENL2.256): LPG lanes x 32 B per row.
+struct F8 { float v[8]; };
+__device__ __forceinline__ F8 ld256(const float* p) {
+    F8 r;
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]), "=f"(r.v[6]),
+                   "=f"(r.v[7])
+                 : "l"(p));
+    return r;
+}
+template <int LPG, int U>
+__global__ void __launch_bounds__(256) ldg256_kernel(const float* __restrict__ Y, const int* __restrict__ idx,
+                                                     int64_t n_idx, float* out) {
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % LPG;
+    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPG;
+    const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / LPG;
+    float acc = 0.f;
+    for (int64_t e = gid; e < n_idx; e += ng * U) {
+        int v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = e + u * ng < n_idx ? __ldg(idx + e + u * ng) : 0;
+        F8 val[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) val[u] = ld256(Y + ((int64_t)v[u] * LPG + gl) * 8);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc += val[u].v[c];
+    }
+    if (acc == 12345.f) out[0] = acc;
+}
+
 // TMA gather4: each warp streams its contiguous slice of idx through S
 // stages of K gather4 (4K rows of ROWB bytes) in shared memory; lane 0
 // issues, every lane consumes (sums) the landed rows.
@@ -168,6 +201,11 @@ static void launch_ldg(void* a_) {
     Args* a = static_cast<Args*>(a_);
     ldg_kernel<LPG, U><<<a->grid, 256>>>(reinterpret_cast<const float4*>(a->Y), a->idx, a->n, a->out);
 }
+template <int LPG, int U>
+static void launch_ldg256(void* a_) {
+    Args* a = static_cast<Args*>(a_);
+    ldg256_kernel<LPG, U><<<a->grid, 256>>>(a->Y, a->idx, a->n, a->out);
+}
 template <int ROWB, int S, int K>
 static void launch_g4(void* a_) {
     Args* a = static_cast<Args*>(a_);
@@ -237,6 +275,18 @@ int main() {
             printf("%-6s ldg  row=%dB LPG=8 U=4 warps/sm %d: %.3f ms %.2f TB/s\n", tag, ROWB, ctas * 8, ms,
                    (double)n_idx * ROWB / (ms * 1e-3) / 1e12);
         }
+        for (int ctas : {4, 8}) {
+            a.grid = nsm * ctas;
+            float ms = time_ms(launch_ldg256<4, 4>, &a);
+            printf("%-6s ldg256 row=%dB LPG=4 U=4 warps/sm %d: %.3f ms %.2f TB/s\n", tag, ROWB, ctas * 8, ms,
+                   (double)n_idx * ROWB / (ms * 1e-3) / 1e12);
+            ms = time_ms(launch_ldg256<4, 8>, &a);
+            printf("%-6s ldg256 row=%dB LPG=4 U=8 warps/sm %d: %.3f ms %.2f TB/s\n", tag, ROWB, ctas * 8, ms,
+                   (double)n_idx * ROWB / (ms * 1e-3) / 1e12);
+            ms = time_ms(launch_ldg<8, 8>, &a);
+            printf("%-6s ldg  row=%dB LPG=8 U=8 warps/sm %d: %.3f ms %.2f TB/s\n", tag, ROWB, ctas * 8, ms,
+                   (double)n_idx * ROWB / (ms * 1e-3) / 1e12);
+        }
         run_g4<ROWB, 4, 2>(a, nsm, 4, tag);
         run_g4<ROWB, 4, 4>(a, nsm, 4, tag);
         run_g4<ROWB, 8, 4>(a, nsm, 4, tag);
@@ -244,6 +294,31 @@ int main() {
         run_g4<ROWB, 8, 8>(a, nsm, 2, tag);
         run_g4<ROWB, 2, 8>(a, nsm, 8, tag);
         run_g4<ROWB, 4, 4>(a, nsm, 8, tag);
+    }
+    // 512-byte rows (config 2): 128-bit vs 256-bit loads, L2-resident and DRAM-random
+    {
+        const int64_t rows512 = y_bytes / 512, hot512 = (32ll << 20) / 512;
+        for (int64_t i = 0; i < n_idx; ++i) h[i] = (int)(rnd() % hot512);
+        CK(cudaMemcpy(idx_hot, h.data(), n_idx * 4, cudaMemcpyHostToDevice));
+        for (int64_t i = 0; i < n_idx; ++i) h[i] = (int)(rnd() % rows512);
+        CK(cudaMemcpy(idx_cold, h.data(), n_idx * 4, cudaMemcpyHostToDevice));
+        a.n = n_idx / 4;
+        for (int pass = 0; pass < 2; ++pass) {
+            a.idx = pass == 0 ? idx_cold : idx_hot;
+            const char* tag = pass == 0 ? "DRAM" : "L2";
+            for (int ctas : {2, 4, 8}) {
+                a.grid = nsm * ctas;
+                float ms = time_ms(launch_ldg<32, 4>, &a);
+                printf("%-6s ldg  row=512B LPG=32 U=4 warps/sm %d: %.3f ms %.2f TB/s\n", tag, ctas * 8, ms,
+                       (double)a.n * 512 / (ms * 1e-3) / 1e12);
+                ms = time_ms(launch_ldg256<16, 4>, &a);
+                printf("%-6s ldg256 row=512B LPG=16 U=4 warps/sm %d: %.3f ms %.2f TB/s\n", tag, ctas * 8, ms,
+                       (double)a.n * 512 / (ms * 1e-3) / 1e12);
+                ms = time_ms(launch_ldg256<16, 2>, &a);
+                printf("%-6s ldg256 row=512B LPG=16 U=2 warps/sm %d: %.3f ms %.2f TB/s\n", tag, ctas * 8, ms,
+                       (double)a.n * 512 / (ms * 1e-3) / 1e12);
+            }
+        }
     }
     printf("done\n");
     return 0;
