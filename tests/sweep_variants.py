@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--small", action="store_true")
     ap.add_argument("--exact", action="store_true")
+    ap.add_argument("--hot", type=int, default=0,
+                    help="characterisation: remap every column to col %% HOT (an L2-resident gather set)")
     a = ap.parse_args()
 
     import torch
@@ -35,6 +37,9 @@ def main():
 
     w = configs.get(a.config, small=a.small)
     A, X, spec, d = w.A, w.X, w.spec, w.d
+    if a.hot:
+        from paper_2011_06391_b200.fusedmm import CsrMatrix
+        A = CsrMatrix(A.nrows, A.ncols, A.row_ptr, A.col_idx % a.hot, A.values)
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
