@@ -272,6 +272,44 @@ __device__ __forceinline__ float group_prod(float v) {
     return v;
 }
 
+// Transposed group reduction of U values over the LPG lanes of a group
+// (U <= LPG, both powers of two): stage k (xor offset LPG >> (k+1)) keeps the
+// lower or upper half of the values a lane carries, by its lane bit, and adds
+// the partner's other half; after log2(U) stages every lane holds the full
+// sum of one value, the remaining stages are a plain butterfly. Lane l ends
+// with value transposed_value(l); every lane holding it has the same bits.
+template <int LPG, int U>
+__device__ __forceinline__ float transposed_sum(const float (&s)[U]) {
+    const int lane = threadIdx.x & 31;
+    float v[U];
+#pragma unroll
+    for (int i = 0; i < U; ++i) v[i] = s[i];
+#pragma unroll
+    for (int n = U, o = LPG / 2; o >= 1; o >>= 1) {
+        if (n > 1) {
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < n / 2; ++i) {
+                const float keep = up ? v[i + n / 2] : v[i];
+                const float send = up ? v[i] : v[i + n / 2];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+            n /= 2;
+        } else {
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+        }
+    }
+    return v[0];
+}
+// Lane offset (within the group) that holds value u after transposed_sum.
+template <int LPG, int U>
+__device__ __forceinline__ constexpr int transposed_lane(int u) {
+    int off = 0;
+    for (int w = U / 2, o = LPG / 2; w >= 1; w >>= 1, o >>= 1)
+        if (u & w) off += o;
+    return off;
+}
+
 // --------------------------------------------------------------- the kernel
 // Per-edge work for U gathered neighbour rows: ROP across the group, SOP,
 // MOP, AOP into z (update_u's loop body, kernel.hpp:92-106).
@@ -315,16 +353,34 @@ __device__ __forceinline__ void consume_edges(const Ops& ops, const KParams& p, 
                 }
                 s[u] = (acc0.x + acc0.y) + (acc1.x + acc1.y);
             }
-            if (LPG > 1) {
+            // h of every edge: with U <= LPG the U partial dots are reduced
+            // "transposed" (each stage halves the values a lane carries, so
+            // U-1 + log2(LPG/U) shuffles instead of U*log2(LPG)), each lane
+            // evaluates the scalar op for one edge, and the U results are
+            // broadcast back; otherwise a butterfly per edge.
+            float hv[U];
+            if constexpr (LPG >= U && U >= 2 && (U & (U - 1)) == 0) {
+                float t = transposed_sum<LPG, U>(s);
+                if (ops.rop() == FMM_ROP_NORM) t = sqrtf(t);
+                const float hl = sop_apply<EXACT>(ops, t, p.alpha, p.k, p.kinv);
+                const int gbase = (threadIdx.x & 31) & ~(LPG - 1);
 #pragma unroll
-                for (int u = 0; u < U; ++u) s[u] = group_sum<LPG>(s[u]);
+                for (int u = 0; u < U; ++u) hv[u] = __shfl_sync(0xffffffffu, hl, gbase + transposed_lane<LPG, U>(u));
+            } else {
+                if (LPG > 1) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) s[u] = group_sum<LPG>(s[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    float sv = s[u];
+                    if (ops.rop() == FMM_ROP_NORM) sv = sqrtf(sv);
+                    hv[u] = sop_apply<EXACT>(ops, sv, p.alpha, p.k, p.kinv);
+                }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                float sv = s[u];
-                if (ops.rop() == FMM_ROP_NORM) sv = sqrtf(sv);
-                float h = sop_apply<EXACT>(ops, sv, p.alpha, p.k, p.kinv);
-                h = ok[u] ? h : 0.0f;
+                float h = ok[u] ? hv[u] : 0.0f;
                 if (ops.mop() == FMM_MOP_MUL_VOP) h *= a[u];
                 const float2 h2 = make_float2(h, h);
 #pragma unroll

@@ -226,9 +226,40 @@ static void run_g4(Args& a, int nsm, int warps_per_cta, const char* tag) {
            (double)a.n * ROWB / (ms * 1e-3) / 1e12);
 }
 
-int main() {
+// File mode: gather 512-byte rows in the order of an int32 index file (e.g.
+// the config 2 CSR column stream written by tools/gather_pattern.py).
+static int file_mode(const char* path, int64_t rows, int nsm) {
+    FILE* f = fopen(path, "rb");
+    if (!f) { perror(path); return 1; }
+    fseek(f, 0, SEEK_END);
+    const int64_t n = ftell(f) / 4;
+    fseek(f, 0, SEEK_SET);
+    std::vector<int> h(n);
+    if (fread(h.data(), 4, n, f) != (size_t)n) { fprintf(stderr, "short read\n"); return 1; }
+    fclose(f);
+    Args a{};
+    float *Y, *out;
+    int* idx;
+    CK(cudaMalloc(&Y, rows * 512));
+    CK(cudaMemset(Y, 0, rows * 512));
+    CK(cudaMalloc(&idx, n * 4));
+    CK(cudaMalloc(&out, 4));
+    CK(cudaMemcpy(idx, h.data(), n * 4, cudaMemcpyHostToDevice));
+    a.Y = Y; a.idx = idx; a.n = n; a.out = out;
+    for (int ctas : {2, 4, 8}) {
+        a.grid = nsm * ctas;
+        float ms = time_ms(launch_ldg<32, 4>, &a);
+        printf("%s ldg128 warps/sm %2d: %.3f ms %.2f TB/s\n", path, ctas * 8, ms, (double)n * 512 / (ms * 1e-3) / 1e12);
+        ms = time_ms(launch_ldg256<16, 4>, &a);
+        printf("%s ldg256 warps/sm %2d: %.3f ms %.2f TB/s\n", path, ctas * 8, ms, (double)n * 512 / (ms * 1e-3) / 1e12);
+    }
+    return 0;
+}
+
+int main(int argc, char** argv) {
     int nsm;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+    if (argc > 2) return file_mode(argv[1], atoll(argv[2]), nsm);
     const int64_t n_idx = 32 << 20;
     const int64_t y_bytes = 1ll << 30;
     float* Y;
