@@ -204,6 +204,28 @@ fmm_status fmm_iterate(fmm_ctx* ctx, const fmm_graph* g,
                        const fmm_opspec* spec, int64_t d, float* X, int iters,
                        uint32_t flags, fmm_stats* stats);
 
+/* ---- one process per GPU: the fused exchange across processes ---------
+ * fmm_run with every final z row also stored into `npeer` (<= 7) peer
+ * buffers: device pointers (FMM_DEVICE_PTRS, single-shard context), each at
+ * the peer's copy of this shard's first row — the next-iterate buffers of
+ * the other ranks, opened with fmm_ipc_open. The slice all-gather of the
+ * iterative workloads then rides on the kernel's own stores (NVLink P2P);
+ * the caller orders the next iteration after every rank's kernel (e.g. a
+ * stream-ordered NCCL barrier). */
+fmm_status fmm_run_peers(fmm_ctx* ctx, const fmm_graph* g,
+                         const fmm_opspec* spec, int64_t d, const float* X,
+                         int64_t ny, const float* Y, float* Z,
+                         float* const* peers, int npeer, uint32_t flags,
+                         fmm_stats* stats);
+
+#define FMM_IPC_HANDLE_BYTES 64
+/* CUDA IPC: export the allocation dptr lies in (handle: FMM_IPC_HANDLE_BYTES
+ * bytes; *offset = dptr - allocation base), map another process's allocation
+ * on `device` (the peer adds the offset), unmap it. */
+fmm_status fmm_ipc_handle(const void* dptr, void* handle, uint64_t* offset);
+fmm_status fmm_ipc_open(const void* handle, int device, void** dptr);
+fmm_status fmm_ipc_close(void* dptr);
+
 /* ---- device-side graph construction ----------- */
 
 /* csr_from_coo on GPU `device` (replaces fusedmm::csr_from_coo,

@@ -74,6 +74,11 @@ SIGNATURES = {
                                   C.c_uint32, C.POINTER(fmm_stats)]),
     "fmm_host_alloc": (C.c_int, [C.POINTER(_P), C.c_size_t]),
     "fmm_host_free": (C.c_int, [_P]),
+    "fmm_run_peers": (C.c_int, [_P, _P, C.POINTER(fmm_opspec), C.c_int64, _P, C.c_int64, _P, _P,
+                                C.POINTER(_P), C.c_int, C.c_uint32, C.POINTER(fmm_stats)]),
+    "fmm_ipc_handle": (C.c_int, [_P, _P, C.POINTER(C.c_uint64)]),
+    "fmm_ipc_open": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
+    "fmm_ipc_close": (C.c_int, [_P]),
     "fmm_csr_from_coo": (C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_int64, _I64P, _I64P, _FP, _I64P,
                                    _I64P, _FP, _I64P]),
     "fmm_csr_sym_unique": (C.c_int, [C.c_int, C.c_int64, C.c_int64, _I64P, _I64P, C.c_int, C.c_int,

@@ -13,6 +13,8 @@
 #include "fmm_sched.cuh"
 #include "fmm_unfused.h"
 
+#include <cuda.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>
@@ -769,9 +771,15 @@ fmm_status fmm_graph_shard_bounds(const fmm_graph* g, int64_t* bounds) {
     return FMM_OK;
 }
 
-fmm_status fmm_run(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec, int64_t d,
-                   const float* X, int64_t ny, const float* Y, float* Z, uint32_t flags,
-                   fmm_stats* stats) {
+}  // extern "C"
+
+namespace {
+
+// fmm_run's body; peers (device pointers, single shard) receive every final
+// z row as well (the fused exchange of fmm_run_peers).
+fmm_status run_impl(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec, int64_t d, const float* X,
+                    int64_t ny, const float* Y, float* Z, uint32_t flags, fmm_stats* stats,
+                    const fmm::PeerOut* peers) {
     if (!ctx || !g || g->ctx != ctx) return FMM_E_INVAL;
     std::lock_guard<std::mutex> lk(ctx->mu);
     fmm_status st = check_spec(ctx, spec, d);
@@ -842,7 +850,7 @@ fmm_status fmm_run(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec, int
         }
         if (timed) FMM_CK(ctx, cudaEventRecord(sh.ev_k0, stream));
         const int l = launch_shard(const_cast<GShard&>(gs), *spec, pattern, d, exact, xd, row0, yd, zd, part,
-                                   gs.val, ctx->variant, sh.num_sms, stream);
+                                   gs.val, ctx->variant, sh.num_sms, stream, dev_ptrs ? peers : nullptr);
         if (l < 0) return set_err(ctx, FMM_E_UNSUPPORTED, "fused_mm: no kernel for this d / alignment");
         launches += l;
         FMM_CK(ctx, cudaGetLastError());
@@ -874,6 +882,83 @@ fmm_status fmm_run(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec, int
         stats->total_ms = tms;
     }
     (void)rows;
+    return FMM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+fmm_status fmm_run(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec, int64_t d,
+                   const float* X, int64_t ny, const float* Y, float* Z, uint32_t flags,
+                   fmm_stats* stats) {
+    return run_impl(ctx, g, spec, d, X, ny, Y, Z, flags, stats, nullptr);
+}
+
+fmm_status fmm_run_peers(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec, int64_t d,
+                         const float* X, int64_t ny, const float* Y, float* Z, float* const* peers,
+                         int npeer, uint32_t flags, fmm_stats* stats) {
+    if (!ctx || !g || g->ctx != ctx) return FMM_E_INVAL;
+    if (!(flags & FMM_DEVICE_PTRS) || ctx->shards.size() != 1)
+        return set_err(ctx, FMM_E_INVAL, "run_peers: device pointers on a single-shard context");
+    if (npeer < 0 || npeer > fmm::kMaxPeers || (npeer > 0 && !peers))
+        return set_err(ctx, FMM_E_INVAL, "run_peers: 0..7 peer buffers");
+    fmm::PeerOut po{};
+    for (int q = 0; q < npeer; ++q) {
+        if (!peers[q]) return set_err(ctx, FMM_E_INVAL, "run_peers: NULL peer buffer");
+        po.p[po.n++] = peers[q];
+    }
+    return run_impl(ctx, g, spec, d, X, ny, Y, Z, flags, stats, &po);
+}
+
+fmm_status fmm_ipc_handle(const void* dptr, void* handle, uint64_t* offset) {
+    if (!dptr || !handle || !offset) return FMM_E_INVAL;
+    // The handle names the whole allocation dptr lies in (a caching
+    // allocator sub-allocates); report dptr's offset from its base.
+    using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static GetRange get_range = nullptr;
+    if (!get_range) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+            cudaGetLastError();
+            return FMM_E_CUDA;
+        }
+        get_range = reinterpret_cast<GetRange>(fn);
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(dptr)) != CUDA_SUCCESS) return FMM_E_CUDA;
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)) != cudaSuccess) {
+        cudaGetLastError();
+        return FMM_E_CUDA;
+    }
+    static_assert(sizeof(h) == FMM_IPC_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle, &h, sizeof(h));
+    *offset = reinterpret_cast<uint64_t>(dptr) - static_cast<uint64_t>(base);
+    return FMM_OK;
+}
+
+fmm_status fmm_ipc_open(const void* handle, int device, void** dptr) {
+    if (!handle || !dptr) return FMM_E_INVAL;
+    *dptr = nullptr;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        return FMM_E_CUDA;
+    }
+    return FMM_OK;
+}
+
+fmm_status fmm_ipc_close(void* dptr) {
+    if (!dptr) return FMM_E_INVAL;
+    if (cudaIpcCloseMemHandle(dptr) != cudaSuccess) {
+        cudaGetLastError();
+        return FMM_E_CUDA;
+    }
     return FMM_OK;
 }
 

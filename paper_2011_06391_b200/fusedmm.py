@@ -274,6 +274,26 @@ def csr_from_coo(entries: Sequence[tuple], m: int, n: int) -> CsrMatrix:
                      np.array(vals, dtype=np.float32))
 
 
+def ipc_handle(dptr: int) -> tuple:
+    """(CUDA IPC handle of the allocation dptr lies in, dptr's offset in it)
+    (fmm_ipc_handle); the peer maps the handle and adds the offset."""
+    buf = C.create_string_buffer(64)
+    off = C.c_uint64()
+    _raise(_lib.lib().fmm_ipc_handle(C.c_void_p(dptr), buf, C.byref(off)))
+    return buf.raw, off.value
+
+
+def ipc_open(handle: bytes, device: int) -> int:
+    """Map another process's allocation on `device` (fmm_ipc_open)."""
+    p = C.c_void_p()
+    _raise(_lib.lib().fmm_ipc_open(C.create_string_buffer(handle, 64), device, C.byref(p)))
+    return p.value
+
+
+def ipc_close(dptr: int) -> None:
+    _raise(_lib.lib().fmm_ipc_close(C.c_void_p(dptr)))
+
+
 def csr_from_coo_device(rows, cols, vals, m: int, n: int, device: int = 0) -> CsrMatrix:
     """csr_from_coo (matrix.hpp:87-140) built on the GPU (fmm_csr_from_coo):
     flat arrays in insertion order; vals None means all ones. Same result and
@@ -522,6 +542,17 @@ class DeviceGraph:
         st = _lib.lib().fmm_run(self.ctx.h, self.h, C.byref(spec.to_c()), d, C.c_void_p(x_ptr), ny,
                                 C.c_void_p(y_ptr), C.c_void_p(z_ptr), flags,
                                 C.byref(stats) if stats is not None else None)
+        _raise(st, self.ctx.h)
+
+    def run_device_peers(self, x_ptr: int, ny: int, y_ptr: int, z_ptr: int, d: int, spec: OpSpec,
+                         peer_ptrs: Sequence[int], flags: int = _lib.FMM_DEVICE_PTRS | _lib.FMM_ASYNC,
+                         stats: Optional[fmm_stats] = None) -> None:
+        """run_device with every final z row also stored into the peer
+        buffers (fmm_run_peers): the fused cross-process exchange."""
+        arr = (C.c_void_p * max(len(peer_ptrs), 1))(*[C.c_void_p(p) for p in peer_ptrs])
+        st = _lib.lib().fmm_run_peers(self.ctx.h, self.h, C.byref(spec.to_c()), d, C.c_void_p(x_ptr), ny,
+                                      C.c_void_p(y_ptr), C.c_void_p(z_ptr), arr, len(peer_ptrs), flags,
+                                      C.byref(stats) if stats is not None else None)
         _raise(st, self.ctx.h)
 
     def run_unfused_device(self, x_ptr: int, ny: int, y_ptr: int, z_ptr: int, d: int, spec: OpSpec,

@@ -27,7 +27,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, cfg, iters, out):
+def _worker(rank, world, port, cfg, iters, out, exchange="broadcast"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -35,7 +35,7 @@ def _worker(rank, world, port, cfg, iters, out):
         from paper_2011_06391_b200 import configs
         from paper_2011_06391_b200.shard import ShardedFusedMM
         w = configs.get(cfg, small=True)
-        sh = ShardedFusedMM(w.A, w.d, w.spec, device=torch.device("cuda", 0))
+        sh = ShardedFusedMM(w.A, w.d, w.spec, device=torch.device("cuda", 0), exchange=exchange)
         X0 = torch.from_numpy(w.X.array.copy()).cuda()
         Z = sh.iterate(X0, iters)
         torch.cuda.synchronize()
@@ -45,13 +45,17 @@ def _worker(rank, world, port, cfg, iters, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("cfg,iters", [(3, 3), (2, 2)])
-def test_sharded_device_iterate_two_ranks(tmp_path, cfg, iters):
+@pytest.mark.parametrize("exchange", ["broadcast", "fused"])
+@pytest.mark.parametrize("cfg,iters,world", [(3, 3, 2), (2, 2, 2), (3, 4, 3)])
+def test_sharded_device_iterate_ranks(tmp_path, cfg, iters, world, exchange):
+    """fused: the kernels of every rank store their z rows into the other
+    ranks' next-X buffers (CUDA IPC mappings, fmm_run_peers); broadcast:
+    post-kernel slice broadcasts. Both bitwise equal to one process."""
     from paper_2011_06391_b200 import configs
     from paper_2011_06391_b200 import fusedmm as F
     from tests.parity import check_exact
     out = str(tmp_path / "z.npy")
-    mp.start_processes(_worker, args=(2, _free_port(), cfg, iters, out), nprocs=2, join=True,
+    mp.start_processes(_worker, args=(world, _free_port(), cfg, iters, out, exchange), nprocs=world, join=True,
                        start_method="spawn")
     w = configs.get(cfg, small=True)
     ref = F.iterate(w.A, w.X, w.spec, iters, 1)
