@@ -241,6 +241,24 @@ fmm_status fmm_csr_from_coo(int device, int64_t m, int64_t n, int64_t count,
                             const float* vals, int64_t* row_ptr,
                             int64_t* col_idx, float* values, int64_t* nnz_out);
 
+/* read_matrix_market (mmio.hpp:23-84): coordinate real|integer|pattern,
+ * general|symmetric, 1-based; pattern values 1, symmetric files mirrored;
+ * parsed on the host with the reference's rules, folded by fmm_csr_from_coo
+ * on GPU `device`. Outputs are malloc'd (release with fmm_free). Parse errors
+ * return FMM_E_INVAL with "<path>:<line>: <what>" in err (the reference's
+ * MmParseError message). */
+fmm_status fmm_read_matrix_market(const char* path, int device, int64_t* m,
+                                  int64_t* n, int64_t* nnz, int64_t** row_ptr,
+                                  int64_t** col_idx, float** values,
+                                  char* err, size_t err_cap);
+/* write_matrix_market (mmio.hpp:87-99): coordinate real general, 1-based,
+ * 17 significant digits. */
+fmm_status fmm_write_matrix_market(const char* path, int64_t m, int64_t n,
+                                   const int64_t* row_ptr,
+                                   const int64_t* col_idx,
+                                   const float* values);
+void fmm_free(void* p);
+
 /* The BASELINE.json graph recipe on GPU `device`: an n x n edge list with
  * self-loops dropped (drop_self), both directions added (symmetrize), sorted
  * and deduplicated; unweighted (a_uv = 1). Host arrays: row_ptr[n+1], col_idx

@@ -88,6 +88,9 @@ def ref_lib() -> C.CDLL:
         L.fmm_ref_rmat.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_uint64,
                                    P64, P64, PF]
         L.fmm_ref_pattern_of.argtypes = [C.POINTER(or_spec)]
+        L.fmm_ref_read_mm.restype = C.c_int64
+        L.fmm_ref_read_mm.argtypes = [C.c_char_p, P64, P64, P64, P64, PF, C.c_int64, C.c_char_p, C.c_int64]
+        L.fmm_ref_write_mm.argtypes = [C.c_char_p, C.c_int64, C.c_int64, P64, P64, PF]
         L.fmm_ref_csr_from_coo.restype = C.c_int64
         L.fmm_ref_csr_from_coo.argtypes = [C.c_int64, C.c_int64, C.c_int64, P64, P64, PF, P64, P64, PF]
         _ref = L
@@ -235,6 +238,32 @@ def ref_csr_from_coo(rows, cols, vals, m: int, n: int):
     if nnz < 0:
         raise ValueError("csr_from_coo: entry out of bounds")
     return rp, cl[:nnz], vl[:nnz]
+
+
+def ref_read_matrix_market(path: str):
+    """The unmodified reference read_matrix_market (mmio.hpp:23-84) as
+    (m, n, row_ptr, col, val); raises ValueError(message) where it throws."""
+    L = ref_lib()
+    m, n = C.c_int64(), C.c_int64()
+    err = C.create_string_buffer(1024)
+    nnz = L.fmm_ref_read_mm(str(path).encode(), C.byref(m), C.byref(n), None, None, None, 0, err, 1024)
+    if nnz < 0:
+        raise ValueError(err.value.decode())
+    rp = np.zeros(m.value + 1, np.int64)
+    cl = np.zeros(max(nnz, 1), np.int64)
+    vl = np.zeros(max(nnz, 1), np.float32)
+    L.fmm_ref_read_mm(str(path).encode(), C.byref(m), C.byref(n), rp.ctypes.data_as(P64), cl.ctypes.data_as(P64),
+                      vl.ctypes.data_as(PF), nnz, err, 1024)
+    return m.value, n.value, rp, cl[:nnz], vl[:nnz]
+
+
+def ref_write_matrix_market(path: str, m: int, n: int, row_ptr, col, val) -> None:
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    cl = np.ascontiguousarray(col, np.int64)
+    vl = np.ascontiguousarray(val, np.float32)
+    if ref_lib().fmm_ref_write_mm(str(path).encode(), m, n, rp.ctypes.data_as(P64), cl.ctypes.data_as(P64),
+                                  vl.ctypes.data_as(PF)) != 0:
+        raise ValueError(f"cannot write {path}")
 
 
 def oracle_csr_from_coo(rows, cols, vals, m: int, n: int):

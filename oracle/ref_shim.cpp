@@ -20,6 +20,7 @@
 
 #include "fusedmm/apps.hpp"
 #include "fusedmm/kernel.hpp"
+#include "fusedmm/mmio.hpp"
 #include "fusedmm/matrix.hpp"
 #include "fusedmm/ops.hpp"
 #include "fusedmm/reference.hpp"
@@ -222,6 +223,46 @@ int64_t fmm_ref_csr_from_coo(int64_t m, int64_t n, int64_t count, const int64_t*
     } catch (const std::exception&) {
         return -1;
     }
+}
+
+// read_matrix_market (mmio.hpp:23-84): returns nnz (filling the buffers
+// when given, capacity cap) or -1 with the exception text in err.
+int64_t fmm_ref_read_mm(const char* path, int64_t* m, int64_t* n, int64_t* row_ptr, int64_t* col, float* val,
+                        int64_t cap, char* err, int64_t err_cap) {
+    try {
+        auto A = read_matrix_market<float>(path);
+        *m = A.nrows;
+        *n = A.ncols;
+        if (row_ptr && A.nnz() <= cap) {
+            std::memcpy(row_ptr, A.row_ptr.data(), sizeof(int64_t) * A.row_ptr.size());
+            std::memcpy(col, A.col_idx.data(), sizeof(int64_t) * A.col_idx.size());
+            std::memcpy(val, A.values.data(), sizeof(float) * A.values.size());
+        }
+        return A.nnz();
+    } catch (const std::exception& e) {
+        if (err && err_cap > 0) {
+            std::strncpy(err, e.what(), static_cast<size_t>(err_cap) - 1);
+            err[err_cap - 1] = '\0';
+        }
+        return -1;
+    }
+}
+
+// write_matrix_market (mmio.hpp:87-99).
+int fmm_ref_write_mm(const char* path, int64_t m, int64_t n, const int64_t* row_ptr, const int64_t* col,
+                     const float* val) {
+    CsrMatrix<float> A;
+    A.nrows = m;
+    A.ncols = n;
+    A.row_ptr.assign(row_ptr, row_ptr + m + 1);
+    A.col_idx.assign(col, col + row_ptr[m]);
+    A.values.assign(val, val + row_ptr[m]);
+    try {
+        write_matrix_market(A, path);
+    } catch (const std::exception&) {
+        return 1;
+    }
+    return 0;
 }
 
 int fmm_ref_pattern_of(const RefSpec* s) {

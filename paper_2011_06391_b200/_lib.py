@@ -81,6 +81,10 @@ SIGNATURES = {
     "fmm_ipc_close": (C.c_int, [_P]),
     "fmm_csr_from_coo": (C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_int64, _I64P, _I64P, _FP, _I64P,
                                    _I64P, _FP, _I64P]),
+    "fmm_read_matrix_market": (C.c_int, [C.c_char_p, C.c_int, _I64P, _I64P, _I64P, C.POINTER(_I64P),
+                                         C.POINTER(_I64P), C.POINTER(_FP), C.c_char_p, C.c_size_t]),
+    "fmm_write_matrix_market": (C.c_int, [C.c_char_p, C.c_int64, C.c_int64, _I64P, _I64P, _FP]),
+    "fmm_free": (None, [_P]),
     "fmm_csr_sym_unique": (C.c_int, [C.c_int, C.c_int64, C.c_int64, _I64P, _I64P, C.c_int, C.c_int,
                                      _I64P, _I64P, _I64P]),
 }

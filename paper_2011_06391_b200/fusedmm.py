@@ -317,6 +317,44 @@ def csr_from_coo_device(rows, cols, vals, m: int, n: int, device: int = 0) -> Cs
     return CsrMatrix(m, n, rp, cl[:k].copy(), vl[:k].copy())
 
 
+class MmParseError(RuntimeError):
+    """mmio.hpp:14-17: '<path>:<line>: <what>'."""
+
+
+def read_matrix_market(path: str, device: int = 0) -> CsrMatrix:
+    """read_matrix_market (mmio.hpp:23-84): parsed on the host with the
+    reference's rules, duplicates folded by csr_from_coo on the GPU."""
+    m, n, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+    rp, cl = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)()
+    vl = C.POINTER(C.c_float)()
+    err = C.create_string_buffer(1024)
+    L = _lib.lib()
+    st = L.fmm_read_matrix_market(str(path).encode(), device, C.byref(m), C.byref(n), C.byref(nnz), C.byref(rp),
+                                  C.byref(cl), C.byref(vl), err, 1024)
+    if st == _lib.FMM_E_INVAL:
+        raise MmParseError(err.value.decode())
+    _raise(st)
+    try:
+        row_ptr = np.ctypeslib.as_array(rp, shape=(m.value + 1,)).copy()
+        k = nnz.value
+        col = np.ctypeslib.as_array(cl, shape=(max(k, 1),))[:k].copy()
+        val = np.ctypeslib.as_array(vl, shape=(max(k, 1),))[:k].copy()
+    finally:
+        for ptr in (rp, cl, vl):
+            L.fmm_free(C.cast(ptr, C.c_void_p))
+    return CsrMatrix(m.value, n.value, row_ptr, col, val)
+
+
+def write_matrix_market(A: CsrMatrix, path: str) -> None:
+    """write_matrix_market (mmio.hpp:87-99)."""
+    rp = np.ascontiguousarray(A.row_ptr, np.int64)
+    cl = np.ascontiguousarray(A.col_idx, np.int64)
+    vl = np.ascontiguousarray(A.values if A.values is not None else np.ones(cl.size), np.float32)
+    st = _lib.lib().fmm_write_matrix_market(str(path).encode(), A.nrows, A.ncols, _i64(rp), _i64(cl), _f32(vl))
+    if st != _lib.FMM_OK:
+        raise RuntimeError(f"cannot write {path}")
+
+
 def csr_sym_unique_device(rows, cols, n: int, drop_self: bool = True, symmetrize: bool = True,
                           device: int = 0) -> CsrMatrix:
     """The BASELINE.json graph recipe on the GPU (fmm_csr_sym_unique): drop

@@ -123,3 +123,73 @@ def test_device_sym_unique_edge_cases():
     assert E.row_ptr.tolist() == [0] * 5 and E.nnz() == 0
     with pytest.raises(F.InvalidArgument):
         F.csr_sym_unique_device([0], [9], 4)
+
+
+# ------------------------------------------------------------ MatrixMarket
+MM_CASES = {
+    "general_real": "%%MatrixMarket matrix coordinate real general\n% comment\n\n3 4 5\n1 2 0.5\n3 4 -1.25e-3\n1 2 2.0\n2 1 7\n3 3 1e10\n",
+    "symmetric_pattern": "%%MatrixMarket matrix coordinate pattern symmetric\n4 4 4\n2 1\n3 1\n4 4\n3 1\n",
+    "integer": "%%MatrixMarket matrix coordinate integer general\n2 2 2\n1 1 3\n2 2 -4\n",
+    "empty": "%%MatrixMarket matrix coordinate real general\n5 5 0\n",
+}
+MM_BAD = {
+    "header": "%%MatrixMarket matrix array real general\n2 2 0\n",
+    "field": "%%MatrixMarket matrix coordinate complex general\n2 2 0\n",
+    "symmetry": "%%MatrixMarket matrix coordinate real hermitian\n2 2 0\n",
+    "size": "%%MatrixMarket matrix coordinate real general\n2 x 0\n",
+    "dims": "%%MatrixMarket matrix coordinate real general\n0 2 0\n",
+    "entry": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1\n",
+    "value": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 abc\n",
+    "bounds": "%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 1.0\n",
+    "count": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n",
+    "empty_file": "",
+}
+
+
+@needs_ref
+@pytest.mark.parametrize("name", sorted(MM_BAD))
+def test_matrix_market_errors_match_reference(tmp_path, name):
+    """Parse errors are detected on the host before any device work, with
+    the reference's MmParseError text."""
+    path = tmp_path / f"{name}.mtx"
+    path.write_text(MM_BAD[name])
+    with pytest.raises(ValueError) as want:
+        oracle.ref_read_matrix_market(path)
+    with pytest.raises(F.MmParseError) as got:
+        F.read_matrix_market(path)
+    assert str(got.value) == str(want.value)
+
+
+@needs_ref
+def test_write_matrix_market_matches_reference_bytes(tmp_path):
+    rng = np.random.default_rng(3)
+    r, c, v = coo_case(3, 30, 20, 200)
+    rp, cl, vl = oracle.ref_csr_from_coo(r, c, v * np.float32(1e-3) - 0.1, 30, 20)
+    A = F.CsrMatrix(30, 20, rp, cl, vl)
+    F.write_matrix_market(A, tmp_path / "ours.mtx")
+    oracle.ref_write_matrix_market(tmp_path / "ref.mtx", 30, 20, rp, cl, vl)
+    assert (tmp_path / "ours.mtx").read_bytes() == (tmp_path / "ref.mtx").read_bytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(MM_CASES))
+def test_device_read_matrix_market_matches_reference(tmp_path, name):
+    path = tmp_path / f"{name}.mtx"
+    path.write_text(MM_CASES[name])
+    A = F.read_matrix_market(path)
+    if oracle.ref_available():
+        m, n, rp, cl, vl = oracle.ref_read_matrix_market(path)
+        assert (A.nrows, A.ncols) == (m, n)
+        same_csr((A.row_ptr, A.col_idx, A.values), (rp, cl, vl))
+    assert F.validate(A) is None
+
+
+@pytest.mark.gpu
+def test_matrix_market_round_trip(tmp_path):
+    """write -> read is the identity on a CSR with unique columns (values
+    printed with 17 significant digits round-trip float32 exactly)."""
+    r, c, v = coo_case(21, 300, 250, 4000)
+    A = F.csr_from_coo_device(r, c, v, 300, 250)
+    F.write_matrix_market(A, tmp_path / "a.mtx")
+    B = F.read_matrix_market(tmp_path / "a.mtx")
+    same_csr((A.row_ptr, A.col_idx, A.values), (B.row_ptr, B.col_idx, B.values))
