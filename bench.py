@@ -51,6 +51,34 @@ def ncu_traffic(cfg: int):
     return None, "no committed ncu capture for this config"
 
 
+def l2_delivery(cfg: int):
+    """(L2->SM bytes per launch of the row kernel from the newest committed
+    ncu capture, the measured delivery ceiling of config 2's own gather
+    stream (tools/gather_pattern.py: plain row gathers of the real CSR column
+    stream, best shape), source) or Nones."""
+    got, src = None, None
+    for path in sorted((ROOT / "profiles").glob("r*_summary.json"), reverse=True):
+        try:
+            s = json.loads(path.read_text())
+        except Exception:
+            continue
+        for name, rep in s.get("reports", {}).items():
+            if name.endswith(f"config{cfg}_rows") and "l1tex__m_xbar2l1tex_read_bytes.sum" in rep:
+                got, src = rep["l1tex__m_xbar2l1tex_read_bytes.sum"], f"{path.name}:{name}"
+                break
+        if got is not None:
+            break
+    ceiling = None
+    if cfg == 2:
+        for path in sorted((ROOT / "profiles").glob("r*_gather_pattern.log"), reverse=True):
+            vals = [float(l.split()[-2]) for l in path.read_text().splitlines()
+                    if l.startswith("/tmp/g_csr.bin") and l.endswith("TB/s")]
+            if vals:
+                ceiling = (max(vals) * 1e3, path.name)
+                break
+    return got, src, ceiling
+
+
 def hbm_peak():
     try:
         p = json.loads(PEAKS_FILE.read_text())
@@ -281,6 +309,16 @@ def run_ours(args):
     mean_ms = kernel_ms_total / args.steps
     achieved = alg / (mean_ms / 1e3) / 1e9
     peak, peak_src = hbm_peak()
+    l2_bytes, l2_src, l2_ceiling = l2_delivery(args.config)
+    delivery = None
+    if l2_bytes is not None:
+        ach = l2_bytes * (nnz_r / max(A.nnz(), 1)) / (mean_ms / 1e3) / 1e9
+        delivery = {"what": "L2->SM bytes of the row kernel (ncu l1tex__m_xbar2l1tex_read_bytes) per launch time",
+                    "achieved": ach, "unit": "GB/s", "bytes_source": l2_src,
+                    "ceiling": l2_ceiling[0] if l2_ceiling else None,
+                    "frac": ach / l2_ceiling[0] if l2_ceiling else None,
+                    "ceiling_source": (f"{l2_ceiling[1]}: plain row gathers of this config's CSR column "
+                                       "stream, best load width / occupancy") if l2_ceiling else None}
 
     # ---- e2e through the C ABI with pinned host buffers
     Xh = F.PinnedBuffer(X.array.shape)  # fmm_host_alloc: page-locked
@@ -333,7 +371,8 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": ncu_traffic(args.config)[0],
                          "traffic_source": ncu_traffic(args.config)[1],
                          "alg_bytes_per_launch": alg, "peak_source": peak_src,
-                         "kernel": "fmm_rows_kernel (+fmm_combine_kernel)"},
+                         "kernel": "fmm_rows_kernel (+fmm_combine_kernel)",
+                         "l2_to_sm": delivery},
             "e2e": {"value": e2e_value, "unit": "nnz*d/s", "h2d_bytes_per_step": int(m * d * 4),
                     "d2h_bytes_per_step": int(rows_r * d * 4), "steps": e2e_steps,
                     "how": "fmm_run(FMM_HOST_PTRS|FMM_ASYNC) pinned host X in / Z out every step, fmm_sync",

@@ -48,10 +48,13 @@ inline bool launch_aligned32(const KParams& p, const Ops& ops, int d, int varian
             launch_one<Ops, 8, 8, 2, 2, EXACT, false>(p, ops, s); return true;
         case 256:
             if constexpr (!EXACT) {
-                if (variant == 21) { launch_one<Ops, 32, 8, 1, 4, EXACT, false>(p, ops, s); return true; }
+                if (variant == 21) { launch_one<Ops, 16, 8, 2, 4, EXACT, false>(p, ops, s); return true; }
                 if (variant == 22) { launch_one<Ops, 8, 8, 4, 2, EXACT, false>(p, ops, s); return true; }
                 if (variant == 23) { launch_one<Ops, 16, 8, 2, 2, EXACT, false>(p, ops, s); return true; }
-                launch_one<Ops, 16, 8, 2, 4, EXACT, false>(p, ops, s); return true;  // config 5
+                if (variant == 24) { launch_one<Ops, 16, 8, 2, 4, EXACT, false, 2>(p, ops, s); return true; }
+                if (variant == 25) { launch_one<Ops, 32, 8, 1, 8, EXACT, false>(p, ops, s); return true; }
+                // config 5: a warp per row-group of 32 lanes x 32 B (80 registers)
+                launch_one<Ops, 32, 8, 1, 4, EXACT, false>(p, ops, s); return true;
             }
             launch_one<Ops, 16, 8, 2, 2, EXACT, false>(p, ops, s); return true;
         default: return false;
