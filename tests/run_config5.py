@@ -1,10 +1,12 @@
-"""Config 5 at full size on one B200 (tool; writes one JSON line).
+"""Config 5 (or config 3 with --config 3) at full size on one B200 (tool;
+writes one JSON line).
 
 R-MAT scale 24, edge factor 32, d=256, ~1.0e9 edges, 5 epochs X <- Z.
 Reports the single-call kernel time, the device-resident 5-epoch loop, and
 teacher-forced parity on sampled rows (hubs included) for the first epochs.
 
     python tests/run_config5.py [--scale 24] [--epochs 5] [--check-epochs 2]
+    python tests/run_config5.py --config 3      # t-distribution layout, 20 iterations
 """
 from __future__ import annotations
 
@@ -22,8 +24,9 @@ sys.path.insert(0, str(ROOT))
 
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=5, choices=(3, 5))
     ap.add_argument("--scale", type=int, default=24)
-    ap.add_argument("--epochs", type=int, default=5)
+    ap.add_argument("--epochs", type=int, default=None)
     ap.add_argument("--check-epochs", type=int, default=2)
     ap.add_argument("--rows", type=int, default=4096)
     a = ap.parse_args()
@@ -35,7 +38,13 @@ def main():
     from tests.parity import check_tolerance
 
     t0 = time.time()
-    w = configs.config5(scale=a.scale, iters=a.epochs)
+    if a.config == 5:
+        a.epochs = a.epochs or 5
+        w = configs.config5(scale=a.scale, iters=a.epochs)
+    else:
+        w = configs.get(3)
+        a.epochs = a.epochs or w.iters
+        a.scale = 21
     gen_s = time.time() - t0
     A, spec, d = w.A, w.spec, w.d
     m, nnz = A.nrows, A.nnz()
