@@ -151,6 +151,15 @@ int fmm_device_count(void);
  * instead of the context's own. stream is a cudaStream_t; NULL means the
  * legacy default stream. fmm_reset_stream restores the context's own. */
 fmm_status fmm_set_stream(fmm_ctx* ctx, int shard, void* stream);
+
+/* Kernel shape variant of this context (the device analogue of the
+ * reference's KernelOptions::lane_width, kernel.hpp:286-288): -1 = the
+ * default shape for d, other values select tuning alternatives (lane-group
+ * width, vector width, unroll, occupancy; unknown values fall back to the
+ * default). fmm_get_variant returns the current one. Initialised from the
+ * FMM_VARIANT environment variable. */
+fmm_status fmm_set_variant(fmm_ctx* ctx, int variant);
+int fmm_get_variant(const fmm_ctx* ctx);
 fmm_status fmm_reset_stream(fmm_ctx* ctx, int shard);
 
 /* Host-side helpers, no device work. */

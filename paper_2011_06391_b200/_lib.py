@@ -58,6 +58,8 @@ SIGNATURES = {
     "fmm_device_count": (C.c_int, []),
     "fmm_set_stream": (C.c_int, [_P, C.c_int, _P]),
     "fmm_reset_stream": (C.c_int, [_P, C.c_int]),
+    "fmm_set_variant": (C.c_int, [_P, C.c_int]),
+    "fmm_get_variant": (C.c_int, [_P]),
     "fmm_pattern_of": (C.c_int, [C.POINTER(fmm_opspec), C.POINTER(C.c_int32)]),
     "fmm_part1d": (C.c_int, [C.c_int64, _I64P, C.c_int, _I64P]),
     "fmm_graph_upload": (C.c_int, [_P, C.c_int64, C.c_int64, _I64P, _I64P, _FP, C.c_int64,

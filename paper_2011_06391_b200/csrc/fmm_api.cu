@@ -592,6 +592,15 @@ fmm_status fmm_set_stream(fmm_ctx* ctx, int shard, void* stream) {
     return FMM_OK;
 }
 
+fmm_status fmm_set_variant(fmm_ctx* ctx, int variant) {
+    if (!ctx || variant < -6 || variant > 63) return FMM_E_INVAL;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->variant = variant;
+    return FMM_OK;
+}
+
+int fmm_get_variant(const fmm_ctx* ctx) { return ctx ? ctx->variant : -1; }
+
 fmm_status fmm_reset_stream(fmm_ctx* ctx, int shard) {
     if (!ctx || shard < 0 || shard >= static_cast<int>(ctx->shards.size())) return FMM_E_INVAL;
     std::lock_guard<std::mutex> lk(ctx->mu);

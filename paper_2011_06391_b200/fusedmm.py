@@ -444,10 +444,12 @@ class KernelStats:
 @dataclass
 class KernelOptions:
     """kernel.hpp:286-288. lane_width is the CPU lane-blocking width; on the
-    device it is validated for interface parity (the lane mapping is fixed
-    by d). exact: None = per-pattern default, True/False = force."""
+    device it is validated for interface parity; the device's own shape
+    choice is `variant` (None = the context's, -1 = default for d; see
+    tune_lane_width). exact: None = per-pattern default, True/False = force."""
     lane_width: int = 8
     exact: Optional[bool] = None
+    variant: Optional[int] = None
 
 
 # ------------------------------------------------------------ ctypes utils
@@ -480,6 +482,12 @@ class Context:
     def sync(self) -> None:
         """Wait for every FMM_ASYNC call enqueued on this context."""
         _raise(_lib.lib().fmm_sync(self.h), self.h)
+
+    def set_variant(self, variant: int) -> None:
+        _raise(_lib.lib().fmm_set_variant(self.h, variant), self.h)
+
+    def variant(self) -> int:
+        return int(_lib.lib().fmm_get_variant(self.h))
 
     def set_stream(self, shard: int, stream_handle: int) -> None:
         _raise(_lib.lib().fmm_set_stream(self.h, shard, C.c_void_p(stream_handle)), self.h)
@@ -675,8 +683,16 @@ def fused_mm(A: CsrMatrix, X: DenseMatrix, Y: DenseMatrix, spec: OpSpec, t: int 
     Xd = X.data if X.data.size else np.zeros(1, np.float32)
     Yd = Y.data if Y.data.size else np.zeros(1, np.float32)
     s = fmm_stats()
-    st = _lib.lib().fmm_run(g.ctx.h, g.h, C.byref(spec.to_c()), X.dim, _vp(Xd), Y.nrows,
-                            _vp(Xd) if Y is X else _vp(Yd), _vp(Z.data), flags, C.byref(s))
+    prev = None
+    if opts is not None and opts.variant is not None:
+        prev = g.ctx.variant()
+        g.ctx.set_variant(opts.variant)
+    try:
+        st = _lib.lib().fmm_run(g.ctx.h, g.h, C.byref(spec.to_c()), X.dim, _vp(Xd), Y.nrows,
+                                _vp(Xd) if Y is X else _vp(Yd), _vp(Z.data), flags, C.byref(s))
+    finally:
+        if prev is not None:
+            g.ctx.set_variant(prev)
     _raise(st, g.ctx.h)
     if stats is not None:
         stats.fill(s)
@@ -699,6 +715,31 @@ def fused_mm_specialized(pattern: KnownPattern, A: CsrMatrix, X: DenseMatrix, Y:
     else:
         raise InvalidArgument("fused_mm_specialized: pattern has no fast path")
     return fused_mm(A, X, X if Y is X else Y, spec, t, None, opts)
+
+
+# shape variants the dispatcher defines (fmm_dispatch.cuh); unknown ones for a
+# given d fall back to its default, so timing them is harmless
+SHAPE_VARIANTS = (-1, 0, 1, 2, 3, 4, 5, 6, 7, 20, 21, 22, 23, 24)
+
+
+def tune_lane_width(A: CsrMatrix, X: DenseMatrix, Y: DenseMatrix, spec: OpSpec, t: int = 1,
+                    repeats: int = 3) -> int:
+    """kernel.hpp:382-402 on the device: times every kernel shape variant for
+    this problem (device time of the fused kernels, after a warm-up) and
+    returns the fastest variant id — pass it back as KernelOptions(variant=…).
+    (The reference returns the fastest CPU lane width in {4, 8, 16}.)"""
+    best, best_ms = -1, float("inf")
+    for v in SHAPE_VARIANTS:
+        opts = KernelOptions(variant=v)
+        fused_mm(A, X, Y, spec, t, None, opts)  # warm-up
+        ms = 0.0
+        for _ in range(repeats):
+            st = KernelStats()
+            fused_mm(A, X, Y, spec, t, st, opts)
+            ms += st.kernel_ms
+        if ms < best_ms:
+            best, best_ms = v, ms
+    return best
 
 
 def iterate(A: CsrMatrix, X: DenseMatrix, spec: OpSpec, iters: int, t: int = 1,

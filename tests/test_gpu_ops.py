@@ -220,3 +220,20 @@ def test_sqk_division_bit_exact_for_every_k(k):
     spec = F.fr_attract_spec(k)
     Z = F.fused_mm(A, X, Y, spec, 1, opts=F.KernelOptions(exact=True))
     check_exact(Z.array, oracle.oracle_fused_mm(A, X, Y, spec))
+
+
+def test_tune_lane_width_and_variant_option():
+    """tune_lane_width (kernel.hpp:382-402) times the device shape variants
+    and returns one; every variant gives the same result within the fast
+    scheme's tolerance (bitwise across runs of one variant)."""
+    A, X, Y = random_case(77, 300, 300, 128, density=0.05, weighted=False)
+    spec = F.make_spec(F.App.NODE_EMBED_SIGMOID)
+    v = F.tune_lane_width(A, X, Y, spec, 1, repeats=1)
+    assert v in F.SHAPE_VARIANTS
+    Z0 = F.fused_mm(A, X, Y, spec, 1, opts=F.KernelOptions(variant=v))
+    Z1 = F.fused_mm(A, X, Y, spec, 1, opts=F.KernelOptions(variant=v))
+    assert np.array_equal(Z0.array, Z1.array)
+    Zo = oracle.oracle_fused_mm(A, X, Y, spec)
+    for var in (-1, 20, 21):
+        Zv = F.fused_mm(A, X, Y, spec, 1, opts=F.KernelOptions(variant=var))
+        check_tolerance(Zv.array, Zo, A, X, Y, spec)
