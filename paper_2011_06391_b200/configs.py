@@ -70,6 +70,16 @@ def rmat_sym(scale: int, edge_factor: int, seed: int) -> CsrMatrix:
     return CsrMatrix(n, n, _take(rp, n + 1, np.int64), _take(cl, nnz.value, np.int64), None)
 
 
+def rmat_generate(scale: int, edge_factor: int = 16, seed: int = 1, device: int = 0) -> CsrMatrix:
+    """rmat_generate (rmat.hpp:24-61): the seeded insertion stream (host,
+    one sequential mt19937_64) folded by csr_from_coo on the GPU — self-loops
+    kept, duplicates summed into values > 1. Bitwise equal to the reference."""
+    from .fusedmm import csr_from_coo_device
+    rows, cols = rmat_stream(scale, edge_factor, seed)
+    n = 1 << scale
+    return csr_from_coo_device(rows, cols, None, n, n, device)
+
+
 def rmat_stream(scale: int, edge_factor: int, seed: int):
     """Raw insertion stream (rows, cols) for cross-checks with the reference."""
     ne = edge_factor << scale

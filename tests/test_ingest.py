@@ -193,3 +193,56 @@ def test_matrix_market_round_trip(tmp_path):
     F.write_matrix_market(A, tmp_path / "a.mtx")
     B = F.read_matrix_market(tmp_path / "a.mtx")
     same_csr((A.row_ptr, A.col_idx, A.values), (B.row_ptr, B.col_idx, B.values))
+
+
+# ---------------------------------------- the reference's own IO tests, ported
+def _mm(tmp_path, name, body):
+    path = tmp_path / name
+    path.write_text(body)
+    return path
+
+
+@pytest.mark.gpu
+def test_ref_io_pattern_symmetric_expands_to_2_cycle(tmp_path):
+    """test_io.cpp:33-43"""
+    A = F.read_matrix_market(_mm(tmp_path, "s.mtx", "%%MatrixMarket matrix coordinate pattern symmetric\n2 2 1\n2 1\n"))
+    assert A.nnz() == 2 and A.row_ptr.tolist() == [0, 1, 2] and A.values.tolist() == [1.0, 1.0]
+
+
+@pytest.mark.gpu
+def test_ref_io_real_general_preserves_weights(tmp_path):
+    """test_io.cpp:45-55"""
+    A = F.read_matrix_market(_mm(tmp_path, "r.mtx", "%%MatrixMarket matrix coordinate real general\n"
+                                 "% a comment\n2 2 2\n1 2 2.5\n2 1 -1.25\n"))
+    assert A.values.tolist() == [2.5, -1.25]
+
+
+def test_ref_io_errors_report_line_and_reject(tmp_path):
+    """test_io.cpp:57-85 (parse errors are raised on the host, no GPU)"""
+    with pytest.raises(F.MmParseError) as e:
+        F.read_matrix_market(_mm(tmp_path, "o.mtx", "%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 1.0\n"))
+    assert ":3:" in str(e.value)
+    with pytest.raises(F.MmParseError):
+        F.read_matrix_market(_mm(tmp_path, "h.mtx", "%%NotMatrixMarket nope\n1 1 0\n"))
+    with pytest.raises(F.MmParseError):
+        F.read_matrix_market(_mm(tmp_path, "v.mtx", "%%MatrixMarket matrix coordinate real general\n1 1 1\n1 1 abc\n"))
+
+
+@pytest.mark.gpu
+def test_ref_io_write_read_round_trips_generated_graph(tmp_path):
+    """test_io.cpp:87-101: rmat_generate (scale 7, ef 4, seed 99) on the
+    device, written and read back unchanged."""
+    A = configs.rmat_generate(7, 4, 99)
+    F.write_matrix_market(A, tmp_path / "rt.mtx")
+    B = F.read_matrix_market(tmp_path / "rt.mtx")
+    assert A.nrows == B.nrows
+    same_csr((A.row_ptr, A.col_idx, A.values), (B.row_ptr, B.col_idx, B.values))
+
+
+@pytest.mark.gpu
+def test_ref_io_rmat_size_contract_and_determinism():
+    """test_io.cpp:103-118"""
+    A = configs.rmat_generate(10, 8, 5)
+    assert A.nrows == 1024 and 0 < A.nnz() <= 8192 and F.validate(A) is None
+    B = configs.rmat_generate(10, 8, 5)
+    same_csr((A.row_ptr, A.col_idx, A.values), (B.row_ptr, B.col_idx, B.values))
