@@ -105,11 +105,18 @@ class ShardedFusedMM:
         dist.all_gather_object(every, mine, group=self.group)
         dev = self.device.index
         # (mapped base, offset) per peer buffer; the mapping is unmapped by base
-        maps = {q: [(F.ipc_open(h, dev), off) for (h, off) in every[q]] for q in range(self.world)
-                if q != self.rank}
-        peers = {q: [base + off for (base, off) in maps[q]] for q in maps}
+        maps: dict = {}
         row_off = self.rb * self.d * 4
         try:
+            # both buffers of a peer may live in one caching-allocator
+            # segment (the same handle): map each distinct handle once
+            for q in range(self.world):
+                if q != self.rank:
+                    maps[q] = {}
+                    for (h, _off) in every[q]:
+                        if h not in maps[q]:
+                            maps[q][h] = F.ipc_open(h, dev)
+            peers = {q: [maps[q][h] + off for (h, off) in every[q]] for q in maps}
             self._barrier()
             for it in range(iters):
                 cur, nxt = bufs[it % 2], bufs[(it + 1) % 2]
@@ -125,7 +132,7 @@ class ShardedFusedMM:
             dist.barrier(group=self.group)  # no rank unmaps while a peer may still store into it
         finally:
             for q in maps:
-                for (base, _off) in maps[q]:
+                for base in maps[q].values():
                     F.ipc_close(base)
         return out
 
