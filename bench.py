@@ -72,7 +72,7 @@ def l2_delivery(cfg: int):
     if cfg == 2:
         for path in sorted((ROOT / "profiles").glob("r*_gather_pattern.log"), reverse=True):
             vals = [float(l.split()[-2]) for l in path.read_text().splitlines()
-                    if l.startswith("/tmp/g_csr.bin") and l.endswith("TB/s")]
+                    if (l.startswith("/tmp/g_csr.bin") or l.startswith("/tmp/g2_csr.bin")) and l.endswith("TB/s")]
             if vals:
                 ceiling = (max(vals) * 1e3, path.name)
                 break

@@ -33,8 +33,9 @@ inline bool launch_aligned32(const KParams& p, const Ops& ops, int d, int varian
                 if (variant == 22) { launch_one<Ops, 4, 8, 1, 8, EXACT, false, 3, 1>(p, ops, s); return true; }
                 if (variant == 23) { launch_one<Ops, 4, 8, 1, 4, EXACT, false, 4, 1>(p, ops, s); return true; }
                 if (variant == 24) { launch_one<Ops, 4, 8, 1, 4, EXACT, false, 3, 1>(p, ops, s); return true; }
+                if (variant == 25) { launch_one<Ops, 4, 8, 1, 2, EXACT, false, 4, 1>(p, ops, s); return true; }
             }
-            // config 3 keeps the VEC = 4 shape (0.649 vs 0.663 ms for VEC = 8)
+            // config 3 keeps the VEC = 4 shape (0.616 ms; VEC = 8 U = 2: 0.618)
             return false;
         case 64:
             launch_one<Ops, 8, 8, 1, 4, EXACT, false>(p, ops, s); return true;  // config 1
@@ -87,8 +88,10 @@ inline bool launch_aligned(const KParams& p, const Ops& ops, int d, int variant,
                 if (variant == 9) { launch_one<Ops, 4, 4, 2, 4, EXACT, false, 4>(p, ops, s); return true; }
                 if (variant == 10) { launch_one<Ops, 4, 4, 2, 4, EXACT, false, 0, 1>(p, ops, s); return true; }
                 if (variant == 11) { launch_one<Ops, 8, 4, 1, 8, EXACT, false, 4, 1>(p, ops, s); return true; }
-                // config 3: 3 blocks/SM with the column prefetch
-                launch_one<Ops, 4, 4, 2, 4, EXACT, false, 3, 1>(p, ops, s); return true;
+                if (variant == 12) { launch_one<Ops, 4, 4, 2, 4, EXACT, false, 3, 1>(p, ops, s); return true; }
+                // config 3: U = 2 at 4 blocks/SM (32 warps) with the column
+                // prefetch (0.616 ms; U = 4 at 3 blocks/SM: 0.646 ms)
+                launch_one<Ops, 4, 4, 2, 2, EXACT, false, 4, 1>(p, ops, s); return true;
             }
             launch_one<Ops, 4, 4, 2, 4, EXACT, false>(p, ops, s); return true;
         case 64:

@@ -228,7 +228,7 @@ static void run_g4(Args& a, int nsm, int warps_per_cta, const char* tag) {
 
 // File mode: gather 512-byte rows in the order of an int32 index file (e.g.
 // the config 2 CSR column stream written by tools/gather_pattern.py).
-static int file_mode(const char* path, int64_t rows, int nsm) {
+static int file_mode(const char* path, int64_t rows, int rowb, int nsm) {
     FILE* f = fopen(path, "rb");
     if (!f) { perror(path); return 1; }
     fseek(f, 0, SEEK_END);
@@ -240,18 +240,29 @@ static int file_mode(const char* path, int64_t rows, int nsm) {
     Args a{};
     float *Y, *out;
     int* idx;
-    CK(cudaMalloc(&Y, rows * 512));
-    CK(cudaMemset(Y, 0, rows * 512));
+    CK(cudaMalloc(&Y, rows * rowb));
+    CK(cudaMemset(Y, 0, rows * rowb));
     CK(cudaMalloc(&idx, n * 4));
     CK(cudaMalloc(&out, 4));
     CK(cudaMemcpy(idx, h.data(), n * 4, cudaMemcpyHostToDevice));
     a.Y = Y; a.idx = idx; a.n = n; a.out = out;
     for (int ctas : {2, 4, 8}) {
         a.grid = nsm * ctas;
-        float ms = time_ms(launch_ldg<32, 4>, &a);
-        printf("%s ldg128 warps/sm %2d: %.3f ms %.2f TB/s\n", path, ctas * 8, ms, (double)n * 512 / (ms * 1e-3) / 1e12);
-        ms = time_ms(launch_ldg256<16, 4>, &a);
-        printf("%s ldg256 warps/sm %2d: %.3f ms %.2f TB/s\n", path, ctas * 8, ms, (double)n * 512 / (ms * 1e-3) / 1e12);
+        float ms1, ms2;
+        if (rowb == 512) {
+            ms1 = time_ms(launch_ldg<32, 4>, &a);
+            ms2 = time_ms(launch_ldg256<16, 4>, &a);
+        } else if (rowb == 128) {
+            ms1 = time_ms(launch_ldg<8, 4>, &a);
+            ms2 = time_ms(launch_ldg256<4, 4>, &a);
+        } else {
+            fprintf(stderr, "row bytes must be 128 or 512\n");
+            return 1;
+        }
+        printf("%s row=%dB ldg128 warps/sm %2d: %.3f ms %.2f TB/s\n", path, rowb, ctas * 8, ms1,
+               (double)n * rowb / (ms1 * 1e-3) / 1e12);
+        printf("%s row=%dB ldg256 warps/sm %2d: %.3f ms %.2f TB/s\n", path, rowb, ctas * 8, ms2,
+               (double)n * rowb / (ms2 * 1e-3) / 1e12);
     }
     return 0;
 }
@@ -259,7 +270,7 @@ static int file_mode(const char* path, int64_t rows, int nsm) {
 int main(int argc, char** argv) {
     int nsm;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
-    if (argc > 2) return file_mode(argv[1], atoll(argv[2]), nsm);
+    if (argc > 2) return file_mode(argv[1], atoll(argv[2]), argc > 3 ? atoi(argv[3]) : 512, nsm);
     const int64_t n_idx = 32 << 20;
     const int64_t y_bytes = 1ll << 30;
     float* Y;
