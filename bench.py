@@ -9,7 +9,8 @@ with the achieved HBM roofline fraction of the fused kernel alongside.
 
 ours:      inputs resident in HBM, kernel timed with CUDA events on the launch
            stream, L2 flushed (256 MiB write) between timed steps outside the
-           events; rows nnz-balanced across ranks with part1d (strong scaling:
+           events; rows split across ranks by part1d balanced on nnz plus a
+           per-row cost (fmm_part1d_weighted; strong scaling:
            the graph is fixed, each rank computes its row block).
            e2e: the same call through the C ABI with pinned HOST buffers
            (X host->device, Z device->host inside the timed region).
@@ -247,7 +248,7 @@ def run_ours(args):
     w, gen_s = load_workload(args.config)
     A, X, spec, d = w.A, w.X, w.spec, w.d
     m = A.nrows
-    plan = F.part1d(A, world)
+    plan = F.shard_bounds(A, world, d)  # part1d balanced on nnz + per-row cost
     rb, re = plan.boundaries[rank], plan.boundaries[rank + 1]
 
     ctx = F.Context([dev.index])
@@ -363,7 +364,7 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded, BASELINE.json recipe)",
             "config": {"workload": w.name, "desc": w.description, "rows": m, "nnz": A.nnz(), "d": d,
-                       "parallelism": f"row-shard x{world} (part1d)",
+                       "parallelism": f"row-shard x{world} (part1d, nnz + per-row cost)",
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "split_rows": int(info.split_rows), "max_degree": int(info.max_degree),
                        "gen_seconds": round(gen_s, 2)},

@@ -168,6 +168,16 @@ fmm_status fmm_pattern_of(const fmm_opspec* spec, int32_t* pattern);
 fmm_status fmm_part1d(int64_t m, const int64_t* row_ptr, int t,
                       int64_t* boundaries);
 
+/* Cost-balanced row partition for GPU shards: boundary i is the smallest row
+ * r with (row_ptr[r] + w*r) * t >= i * (nnz + w*m) — each row also costs w
+ * edge-equivalents of per-row kernel work; w = 0 is exactly fmm_part1d. The
+ * result is bitwise independent of the partition (rows are never split). */
+fmm_status fmm_part1d_weighted(int64_t m, const int64_t* row_ptr, int t,
+                               double row_weight, int64_t* boundaries);
+/* Row weight fmm_graph_upload uses to split a multi-shard context's rows
+ * (default 0: the reference's part1d). */
+fmm_status fmm_set_row_weight(fmm_ctx* ctx, double row_weight);
+
 /* Upload A (CSR, host arrays, int64 indices as in matrix.hpp:48-68).
  * Only rows [row_begin, row_end) are uploaded (pass 0, m for all rows); a
  * multi-shard context further splits that range with part1d. values may be

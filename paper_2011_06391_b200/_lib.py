@@ -62,6 +62,8 @@ SIGNATURES = {
     "fmm_get_variant": (C.c_int, [_P]),
     "fmm_pattern_of": (C.c_int, [C.POINTER(fmm_opspec), C.POINTER(C.c_int32)]),
     "fmm_part1d": (C.c_int, [C.c_int64, _I64P, C.c_int, _I64P]),
+    "fmm_part1d_weighted": (C.c_int, [C.c_int64, _I64P, C.c_int, C.c_double, _I64P]),
+    "fmm_set_row_weight": (C.c_int, [_P, C.c_double]),
     "fmm_graph_upload": (C.c_int, [_P, C.c_int64, C.c_int64, _I64P, _I64P, _FP, C.c_int64,
                                    C.c_int64, C.POINTER(_P)]),
     "fmm_graph_free": (C.c_int, [_P]),

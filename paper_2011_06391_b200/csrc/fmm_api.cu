@@ -59,6 +59,7 @@ struct Shard {
 struct fmm_ctx {
     std::vector<Shard> shards;
     int variant = -1;  // kernel shape variant (FMM_VARIANT env, tuning only)
+    double row_weight = 0.0;  // shard partition: 0 = part1d, > 0 = part1d_weighted
     bool p2p_ok = true;  // every pair of distinct shard devices has peer access
     std::string err;
     std::mutex mu;
@@ -615,6 +616,25 @@ fmm_status fmm_pattern_of(const fmm_opspec* spec, int32_t* pattern) {
     return FMM_OK;
 }
 
+fmm_status fmm_part1d_weighted(int64_t m, const int64_t* row_ptr, int t, double row_weight,
+                               int64_t* boundaries) {
+    if (m < 0 || !row_ptr || !boundaries || t < 1 || !(row_weight >= 0.0)) return FMM_E_INVAL;
+    try {
+        const auto b = fmm::part1d_weighted(m, row_ptr, t, row_weight);
+        std::memcpy(boundaries, b.data(), b.size() * sizeof(int64_t));
+    } catch (const std::exception&) {
+        return FMM_E_INVAL;
+    }
+    return FMM_OK;
+}
+
+fmm_status fmm_set_row_weight(fmm_ctx* ctx, double row_weight) {
+    if (!ctx || !(row_weight >= 0.0)) return FMM_E_INVAL;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->row_weight = row_weight;
+    return FMM_OK;
+}
+
 fmm_status fmm_part1d(int64_t m, const int64_t* row_ptr, int t, int64_t* boundaries) {
     if (m < 0 || !row_ptr || !boundaries || t < 1) return FMM_E_INVAL;
     try {
@@ -654,7 +674,7 @@ fmm_status fmm_graph_upload(fmm_ctx* ctx, int64_t m, int64_t n, const int64_t* r
     // part1d over the requested row range (kernel.hpp:24-49)
     std::vector<int64_t> bounds;
     try {
-        bounds = fmm::part1d(row_end - row_begin, row_ptr + row_begin, S);
+        bounds = fmm::part1d_weighted(row_end - row_begin, row_ptr + row_begin, S, ctx->row_weight);
     } catch (const std::exception& e) {
         delete g;
         return set_err(ctx, FMM_E_INVAL, e.what());

@@ -29,6 +29,23 @@ std::vector<int64_t> part1d(int64_t m, const int64_t* row_ptr, int t) {
     return b;
 }
 
+std::vector<int64_t> part1d_weighted(int64_t m, const int64_t* row_ptr, int t, double w) {
+    if (!(w > 0.0)) return part1d(m, row_ptr, t);
+    if (t < 1) throw std::invalid_argument("part1d: worker count must be >= 1");
+    std::vector<int64_t> b(static_cast<size_t>(t) + 1, 0);
+    b[t] = m;
+    const int64_t base = row_ptr[0];
+    const long double total = static_cast<long double>(row_ptr[m] - base) + static_cast<long double>(w) * m;
+    int64_t row = 0;
+    for (int i = 1; i < t; ++i) {
+        const long double target = total * i / t;
+        while (row < m && static_cast<long double>(row_ptr[row] - base) + static_cast<long double>(w) * row < target)
+            ++row;
+        b[i] = row;
+    }
+    return b;
+}
+
 std::string validate_row_ptr(int64_t m, const int64_t* row_ptr) {
     if (m < 0) return "negative row count";
     if (row_ptr[0] != 0) return "row_ptr[0] != 0";

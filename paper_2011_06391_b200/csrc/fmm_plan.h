@@ -29,6 +29,12 @@ struct Int4 {
 // applied to row_ptr[r] - row_ptr[0]).
 std::vector<int64_t> part1d(int64_t m, const int64_t* row_ptr, int t);
 
+// Cost-balanced variant for GPU shards: boundary i is the smallest row r with
+// (row_ptr[r] + w*r) * t >= i * (nnz + w*m), i.e. every row also costs w
+// edge-equivalents (the per-row work of the row kernels: descriptor, x_u,
+// z_u, the first-batch latency). w == 0 is exactly part1d.
+std::vector<int64_t> part1d_weighted(int64_t m, const int64_t* row_ptr, int t, double w);
+
 // Validates row_ptr over [row_begin, row_end]: monotone, row_ptr[0] == 0.
 // Returns an empty string when valid, else the first violation.
 std::string validate_row_ptr(int64_t m, const int64_t* row_ptr);

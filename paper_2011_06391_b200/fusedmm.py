@@ -420,6 +420,23 @@ def part1d(A: CsrMatrix, t: int) -> PartitionPlan:
     return PartitionPlan([int(x) for x in b], t)
 
 
+def row_weight_for(d: int) -> float:
+    """Per-row kernel cost in edge-equivalents for dimension d (fitted on
+    configs 2 and 3: ~6 at d=128, ~3.6 at d=32; tools/shard_balance.py)."""
+    return 2.0 + d / 32.0
+
+
+def shard_bounds(A: CsrMatrix, t: int, d: int) -> PartitionPlan:
+    """Row blocks for t GPU shards: part1d balanced on nnz + w(d) per row
+    (fmm_part1d_weighted) so the shards' kernel times, not just their edge
+    counts, match. Results are bitwise independent of the partition."""
+    if t < 1:
+        raise InvalidArgument("part1d: worker count must be >= 1")
+    b = np.zeros(t + 1, dtype=np.int64)
+    _raise(_lib.lib().fmm_part1d_weighted(A.nrows, _i64(A.row_ptr), t, row_weight_for(d), _i64(b)))
+    return PartitionPlan([int(x) for x in b], t)
+
+
 @dataclass
 class KernelStats:
     """kernel.hpp:51-55 (+ device evidence)."""
@@ -482,6 +499,10 @@ class Context:
     def sync(self) -> None:
         """Wait for every FMM_ASYNC call enqueued on this context."""
         _raise(_lib.lib().fmm_sync(self.h), self.h)
+
+    def set_row_weight(self, w: float) -> None:
+        """Row weight of the shard partition for graphs uploaded afterwards."""
+        _raise(_lib.lib().fmm_set_row_weight(self.h, w), self.h)
 
     def set_variant(self, variant: int) -> None:
         _raise(_lib.lib().fmm_set_variant(self.h, variant), self.h)

@@ -3,7 +3,8 @@
 The reference's only parallelism is t std::thread workers over part1d row
 ranges with X/Z partitioned and Y shared read-only (kernel.hpp:290-345,
 PAPER.md:480-496). Here each rank is one GPU: rank r owns rows
-[b_r, b_{r+1}) of part1d(A, world), holds X (= Y) replicated in HBM and
+[b_r, b_{r+1}) of part1d(A, world) balanced on nnz plus a per-row cost
+(fmm_part1d_weighted), holds X (= Y) replicated in HBM and
 computes its Z slice with the fused kernel — no collective on the data path.
 Iterative workloads (configs 3 and 5: X <- Z) exchange the fresh Z slices
 between iterations. Default on GPUs ("fused"): the ranks map each other's
@@ -27,7 +28,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from .fusedmm import CsrMatrix, Context, DeviceGraph, OpSpec, part1d
+from .fusedmm import CsrMatrix, Context, DeviceGraph, OpSpec, shard_bounds
 
 # compute(X_full, Y_full, row_begin, row_end) -> Z slice (row_end-row_begin, d)
 ComputeFn = Callable[[torch.Tensor, torch.Tensor, int, int], torch.Tensor]
@@ -41,7 +42,9 @@ class ShardedFusedMM:
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.A, self.d, self.spec = A, d, spec
-        self.bounds = part1d(A, self.world).boundaries
+        # cost-balanced part1d (nnz + w(d) per row): rows are never split, so
+        # the result is bitwise independent of the partition
+        self.bounds = shard_bounds(A, self.world, d).boundaries
         self.rb, self.re = self.bounds[self.rank], self.bounds[self.rank + 1]
         self.launches = 0
         if exchange not in ("fused", "broadcast"):

@@ -133,3 +133,32 @@ def test_headers_compile_as_c_and_cpp(tmp_path):
                         f"-L{_lib.LIB_PATH.parent}", "-lfusedmm_cuda", "-o", str(tmp_path / "demo")],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_part1d_weighted(seed):
+    """w = 0 is exactly part1d; w > 0 balances nnz + w per row: every block's
+    cost is within one row's cost of the ideal split."""
+    rng = np.random.default_rng(100 + seed)
+    m = int(rng.integers(1, 400))
+    deg = rng.integers(0, 40, m) * (rng.random(m) < 0.7)
+    row_ptr = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+    A = F.CsrMatrix(m, m, row_ptr, np.zeros(int(row_ptr[-1]), np.int64), None)
+    L = _lib.lib()
+    for t in (1, 2, 3, 8):
+        b = np.zeros(t + 1, np.int64)
+        assert L.fmm_part1d_weighted(m, row_ptr.ctypes.data_as(C.POINTER(C.c_int64)), t, 0.0,
+                                     b.ctypes.data_as(C.POINTER(C.c_int64))) == _lib.FMM_OK
+        assert b.tolist() == F.part1d(A, t).boundaries
+        for w in (1.0, 6.0):
+            b = np.zeros(t + 1, np.int64)
+            L.fmm_part1d_weighted(m, row_ptr.ctypes.data_as(C.POINTER(C.c_int64)), t, w,
+                                  b.ctypes.data_as(C.POINTER(C.c_int64)))
+            cost = row_ptr + w * np.arange(m + 1)
+            assert b[0] == 0 and b[-1] == m and np.all(np.diff(b) >= 0)
+            for i in range(1, t):
+                r = b[i]
+                assert cost[r] * t >= i * cost[m] - 1e-9
+                assert r == 0 or cost[r - 1] * t < i * cost[m]
+    assert L.fmm_part1d_weighted(m, row_ptr.ctypes.data_as(C.POINTER(C.c_int64)), 2, -1.0,
+                                 np.zeros(3, np.int64).ctypes.data_as(C.POINTER(C.c_int64))) == _lib.FMM_E_INVAL

@@ -66,8 +66,8 @@ def test_two_rank_iterate_bitwise_equals_single(tmp_path, cfg, iters):
         X = F.DenseMatrix.wrap(oracle.oracle_fused_mm(w.A, X, X, w.spec))
     assert np.array_equal(res["Z"].view(np.uint32), X.array.view(np.uint32))
     b = res["bounds"].tolist()
-    assert b == F.part1d(w.A, 2).boundaries
-    # each rank's one-step slice is its part1d row block of the full result
+    assert b == F.shard_bounds(w.A, 2, w.d).boundaries
+    # each rank's one-step slice is its row block of the full result
     Z1 = oracle.oracle_fused_mm(w.A, w.X, w.X, w.spec)
     for r in range(2):
         s = np.load(f"{out}.step{r}.npy")
