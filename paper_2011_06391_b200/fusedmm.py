@@ -650,13 +650,16 @@ class DeviceGraph:
             pass
 
 
-def _device_graph(A: CsrMatrix, t: int) -> DeviceGraph:
+def _device_graph(A: CsrMatrix, t: int, d: int = 0) -> DeviceGraph:
     key = (t, A.row_ptr.ctypes.data, A.col_idx.ctypes.data, A.values.ctypes.data, A.nnz())
     g = A._device.get(t)
     if g is None or g._key != key:
         if g is not None:
             g.free()
-        g = DeviceGraph(default_context(t), A)
+        ctx = default_context(t)
+        if t > 1:  # shards balanced on nnz + the per-row cost for this d
+            ctx.set_row_weight(row_weight_for(d) if d > 0 else 0.0)
+        g = DeviceGraph(ctx, A)
         g._key = key
         A._device[t] = g
     return g
@@ -700,7 +703,7 @@ def fused_mm(A: CsrMatrix, X: DenseMatrix, Y: DenseMatrix, spec: OpSpec, t: int 
         if stats is not None:
             stats.threads, stats.pattern = t, pattern_of(spec)
         return Z
-    g = _device_graph(A, t)
+    g = _device_graph(A, t, X.dim)
     Xd = X.data if X.data.size else np.zeros(1, np.float32)
     Yd = Y.data if Y.data.size else np.zeros(1, np.float32)
     s = fmm_stats()
@@ -774,7 +777,7 @@ def iterate(A: CsrMatrix, X: DenseMatrix, spec: OpSpec, iters: int, t: int = 1,
     out = DenseMatrix.wrap(X.array.copy())
     if A.nrows == 0:
         return out
-    g = _device_graph(A, t)
+    g = _device_graph(A, t, X.dim)
     s = g.iterate_host(out.data, X.dim, spec, iters, _flags(opts))
     if stats is not None:
         stats.fill(s)

@@ -126,3 +126,20 @@ def test_fused_exchange_iterate(cfg):
         X = w.X.array.copy()
         g.iterate_host(X, w.d, w.spec, iters, flags)
         check_exact(X, ref.array)
+
+
+def test_weighted_shards_bitwise_equal():
+    """The cost-balanced shard partition (fmm_set_row_weight) moves row
+    boundaries only: Z is bitwise identical to one shard."""
+    w = configs.get(2, small=True)
+    Z1 = F.fused_mm(w.A, w.X, w.X, w.spec, 1)
+    for t in (2, 3):
+        ctx = F.Context([0] * t)
+        ctx.set_row_weight(F.row_weight_for(w.d))
+        g = F.DeviceGraph(ctx, w.A)
+        assert g.shard_bounds() == F.shard_bounds(w.A, t, w.d).boundaries
+        assert g.shard_bounds() != F.part1d(w.A, t).boundaries
+        Zt = np.zeros_like(Z1.array)
+        g.run_host(w.X.array, w.X.array, Zt, w.d, w.spec)
+        check_exact(Zt, Z1.array)
+    check_exact(F.fused_mm(w.A, w.X, w.X, w.spec, 3).array, Z1.array)
