@@ -421,9 +421,11 @@ def part1d(A: CsrMatrix, t: int) -> PartitionPlan:
 
 
 def row_weight_for(d: int) -> float:
-    """Per-row kernel cost in edge-equivalents for dimension d (fitted on
-    configs 2 and 3: ~6 at d=128, ~3.6 at d=32; tools/shard_balance.py)."""
-    return 2.0 + d / 32.0
+    """Per-row kernel cost in edge-equivalents for dimension d, from fits of
+    the measured shard times (tools/shard_balance.py): ~3.6 at d=32 (config
+    3), ~6 at d=128 (config 2), ~3.3 at d=256 (config 5, where the 8-shard
+    speed-up is flat for w in 2..10)."""
+    return min(8.0, 2.5 + d / 32.0)
 
 
 def shard_bounds(A: CsrMatrix, t: int, d: int) -> PartitionPlan:
