@@ -90,6 +90,7 @@ struct GShard {
     int4* items = nullptr;
     int4* chunks = nullptr;
     int4* split_rows = nullptr;
+    unsigned* split_count = nullptr;  // in-kernel fold tickets (zero between launches)
 };
 
 }  // namespace
@@ -348,9 +349,18 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
         }
     }
     if (variant < -1) variant = -1;
+    // split rows fold inside the row kernel (the last chunk's warp) unless
+    // FMM_FOLD_KERNEL selects the separate combine kernel
+    static const bool fold_kernel = std::getenv("FMM_FOLD_KERNEL") != nullptr;
+    const bool inline_fold = split && gs.split_count != nullptr && !fold_kernel;
+    if (inline_fold) {
+        p.split_rows = gs.split_rows;
+        p.split_count = gs.split_count;
+        p.fold_max = spec.aop == FMM_AOP_AMAX ? 1 : 0;
+    }
     if (!launch_rows(p, pattern, static_cast<int>(d), exact, a32, a16, a8, variant, stream)) return -1;
     int launches = 1;
-    if (split && gs.n_split_rows > 0) {
+    if (split && gs.n_split_rows > 0 && !inline_fold) {
         fmm::fmm_combine_kernel<<<static_cast<unsigned>(gs.n_split_rows), 256, 0, stream>>>(
             gs.split_rows, partial, Z, static_cast<int>(d), spec.aop == FMM_AOP_AMAX ? 1 : 0, po);
         ++launches;
@@ -713,6 +723,11 @@ fmm_status fmm_graph_upload(fmm_ctx* ctx, int64_t m, int64_t n, const int64_t* r
         std::memcpy(sr.data(), P.split_rows.data(), sr.size() * sizeof(int4));
         if ((st = upload_vec(ctx, ch, &gs.chunks)) != FMM_OK) break;
         if ((st = upload_vec(ctx, sr, &gs.split_rows)) != FMM_OK) break;
+        if (!sr.empty()) {
+            cudaError_t e = cudaMalloc(&gs.split_count, sr.size() * sizeof(unsigned));
+            if (e == cudaSuccess) e = cudaMemset(gs.split_count, 0, sr.size() * sizeof(unsigned));
+            if (e != cudaSuccess) { st = cuda_err(ctx, e, "split counters"); break; }
+        }
         if (gs.nnz > 0) {
             // narrow + validate columns in staged slices
             auto fail = [&](cudaError_t e, const char* w) { st = cuda_err(ctx, e, w); };
@@ -766,6 +781,7 @@ fmm_status fmm_graph_free(fmm_graph* g) {
                 if (q) cudaFree(q);
         for (void* p : {static_cast<void*>(gs.row_ptr), static_cast<void*>(gs.col), static_cast<void*>(gs.val),
                         static_cast<void*>(gs.order), static_cast<void*>(gs.items), static_cast<void*>(gs.chunks),
+                        static_cast<void*>(gs.split_count),
                         static_cast<void*>(gs.split_rows)})
             if (p) cudaFree(p);
     }

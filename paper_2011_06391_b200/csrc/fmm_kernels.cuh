@@ -49,7 +49,12 @@ struct KParams {
     const int32_t* order;    // rows, heavy first: wide rows then narrow rows
     const int4* items;       // per order slot {row, e0 lo, e0 hi, degree}: one
                              // load replaces order[i] -> row_ptr[r], row_ptr[r+1]
-    const int4* chunks;      // chunk items {row, k, slot, 0}
+    const int4* chunks;      // chunk items {row, k, slot, split-row index}
+    // in-kernel chunk fold: the warp finishing a split row's last chunk
+    // (ticket from split_count) folds the row's partials in chunk order
+    const int4* split_rows;  // {row, first slot, nchunks, 0}
+    unsigned* split_count;   // per split row, zero between launches; nullptr: fold kernel
+    int fold_max;            // AOP is AMAX
     int64_t n_chunk_items;
     int64_t n_wide_rows;     // rows a whole warp folds (edges over its groups)
     int64_t n_narrow_rows;   // rows one lane group folds
@@ -661,6 +666,60 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
                     for (int q = 0; q < p.n_peer; ++q)
                         store_vec<VEC>(p.zpeer[q] + r * d + (i * LPG + gl) * VEC, &z[i * VEC]);
             }
+        if (!to_peers && p.split_count != nullptr) {
+            // last chunk of the row to finish folds all its partials, in
+            // chunk order per element (deterministic, shard-independent)
+            const int si = p.chunks[warp].w;
+            const int4 sr = p.split_rows[si];
+            __threadfence();  // this warp's partial is visible device-wide
+            unsigned ticket = 0;
+            if (lane == 0) ticket = atomicAdd(p.split_count + si, 1u);
+            ticket = __shfl_sync(0xffffffffu, ticket, 0);
+            if (ticket + 1 == static_cast<unsigned>(sr.z)) {
+                __threadfence();  // acquire: every partial of the row is visible
+                const float* base = p.partial + static_cast<int64_t>(sr.y) * d;
+                float* zr = p.Z + static_cast<int64_t>(sr.x) * d;
+                const float id = aop_identity(ops);
+                const bool mx = p.fold_max != 0;
+                auto f1 = [&](float a, float v) { return mx ? (a < v ? v : a) : __fadd_rn(a, v); };
+                if ((d & 3) == 0) {
+                    // float4 per lane, 8 chunks in flight; per element the
+                    // chunks fold in order
+                    const int d4 = d >> 2;
+                    for (int j4 = lane; j4 < d4; j4 += 32) {
+                        float4 acc = make_float4(id, id, id, id);
+                        int k = 0;
+                        for (; k + 8 <= sr.z; k += 8) {
+                            float4 v[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                v[q] = __ldcg(reinterpret_cast<const float4*>(base + static_cast<int64_t>(k + q) * d) + j4);
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                acc.x = f1(acc.x, v[q].x); acc.y = f1(acc.y, v[q].y);
+                                acc.z = f1(acc.z, v[q].z); acc.w = f1(acc.w, v[q].w);
+                            }
+                        }
+                        for (; k < sr.z; ++k) {
+                            const float4 v = __ldcg(reinterpret_cast<const float4*>(base + static_cast<int64_t>(k) * d) + j4);
+                            acc.x = f1(acc.x, v.x); acc.y = f1(acc.y, v.y);
+                            acc.z = f1(acc.z, v.z); acc.w = f1(acc.w, v.w);
+                        }
+                        reinterpret_cast<float4*>(zr)[j4] = acc;
+                        for (int q = 0; q < p.n_peer; ++q)
+                            reinterpret_cast<float4*>(p.zpeer[q] + static_cast<int64_t>(sr.x) * d)[j4] = acc;
+                    }
+                } else {
+                    for (int j = lane; j < d; j += 32) {
+                        float acc = id;
+                        for (int k = 0; k < sr.z; ++k) acc = f1(acc, __ldcg(base + static_cast<int64_t>(k) * d + j));
+                        zr[j] = acc;
+                        for (int q = 0; q < p.n_peer; ++q) p.zpeer[q][static_cast<int64_t>(sr.x) * d + j] = acc;
+                    }
+                }
+                if (lane == 0) p.split_count[si] = 0;  // ready for the next launch
+            }
+        }
         return;
     }
 

@@ -119,9 +119,10 @@ ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t ro
         const int64_t deg = P.local_row_ptr[r + 1] - P.local_row_ptr[r];
         const int64_t nch = (deg + kChunkEdges - 1) / kChunkEdges;
         if (slot + nch > INT32_MAX) throw std::invalid_argument("too many chunk slots");
+        const int32_t si = static_cast<int32_t>(P.split_rows.size());
         P.split_rows.push_back({r, static_cast<int32_t>(slot), static_cast<int32_t>(nch), 0});
         for (int64_t k = 0; k < nch; ++k)
-            P.chunks.push_back({r, static_cast<int32_t>(k), static_cast<int32_t>(slot + k), 0});
+            P.chunks.push_back({r, static_cast<int32_t>(k), static_cast<int32_t>(slot + k), si});
         slot += nch;
     }
     P.n_slots = slot;

@@ -54,7 +54,7 @@ struct ShardPlan {
     std::vector<Int4> items;
     int64_t n_split_rows = 0;             // prefix of `order` cut into chunks
     int64_t n_wide_rows = 0;              // next rows with degree >= kWideMin
-    std::vector<Int4> chunks;             // {row, k, slot, 0}
+    std::vector<Int4> chunks;             // {row, k, slot, split-row index}
     std::vector<Int4> split_rows;         // {row, first slot, nchunks, 0}
     int64_t n_slots = 0;
     int64_t nonempty_rows = 0;
