@@ -372,7 +372,7 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": ncu_traffic(args.config)[0],
                          "traffic_source": ncu_traffic(args.config)[1],
                          "alg_bytes_per_launch": alg, "peak_source": peak_src,
-                         "kernel": "fmm_rows_kernel (+fmm_combine_kernel)",
+                         "kernel": "fmm_rows_kernel (split-row chunks folded in-kernel)",
                          "l2_to_sm": delivery},
             "e2e": {"value": e2e_value, "unit": "nnz*d/s", "h2d_bytes_per_step": int(m * d * 4),
                     "d2h_bytes_per_step": int(rows_r * d * 4), "steps": e2e_steps,
