@@ -267,7 +267,7 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
     p.Z = Z;
     p.partial = partial;
     p.row0 = row0;
-    p.chunk = fmm::kChunkEdges;
+    p.chunk = gs.plan ? gs.plan->chunk : 256;
     p.d = static_cast<int>(d);
     p.vop = spec.vop; p.rop = spec.rop; p.sop = spec.sop; p.mop = spec.mop; p.aop = spec.aop;
     p.alpha = spec.alpha;
@@ -690,6 +690,9 @@ fmm_status fmm_graph_upload(fmm_ctx* ctx, int64_t m, int64_t n, const int64_t* r
         return set_err(ctx, FMM_E_INVAL, e.what());
     }
     g->shards.resize(S);
+    // chunk size from the whole matrix (never the uploaded range or a shard):
+    // per-rank uploads of one graph must split rows identically
+    const int chunk = fmm::choose_chunk_edges(row_ptr[m] - row_ptr[0]);
     fmm_status st = FMM_OK;
     for (int s = 0; s < S && st == FMM_OK; ++s) {
         GShard& gs = g->shards[s];
@@ -699,7 +702,7 @@ fmm_status fmm_graph_upload(fmm_ctx* ctx, int64_t m, int64_t n, const int64_t* r
         gs.row_end = row_begin + bounds[s + 1];
         fmm::ShardPlan P;
         try {
-            P = fmm::build_shard_plan(row_ptr, gs.row_begin, gs.row_end);
+            P = fmm::build_shard_plan(row_ptr, gs.row_begin, gs.row_end, chunk);
         } catch (const std::exception& e) {
             st = set_err(ctx, FMM_E_UNSUPPORTED, e.what());
             break;

@@ -2,11 +2,22 @@
 #include "fmm_plan.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <functional>
 #include <queue>
 #include <stdexcept>
 
 namespace fmm {
+
+int choose_chunk_edges(int64_t total_nnz) {
+    if (const char* e = std::getenv("FMM_CHUNK")) {
+        const int v = std::atoi(e);
+        if (v >= 32) return v;
+    }
+    int c = 256;
+    while (c < 16384 && static_cast<int64_t>(c) * 8192 * 3 / 2 < total_nnz) c *= 2;
+    return c;
+}
 
 std::vector<int64_t> part1d(int64_t m, const int64_t* row_ptr, int t) {
     if (t < 1) throw std::invalid_argument("part1d: worker count must be >= 1");
@@ -69,8 +80,9 @@ inline int degree_bucket(int64_t deg) {
 }
 }  // namespace
 
-ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t row_end) {
+ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t row_end, int chunk) {
     ShardPlan P;
+    P.chunk = chunk;
     P.row_begin = row_begin;
     P.row_end = row_end;
     P.edge_begin = row_ptr[row_begin];
@@ -86,7 +98,7 @@ ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t ro
     std::vector<int64_t> count(kKeys + 1, 0);
     auto key_of = [&](int64_t r) {
         const int64_t deg = P.local_row_ptr[r + 1] - P.local_row_ptr[r];
-        const int split = deg > kChunkEdges ? 1 : 0;
+        const int split = deg > P.chunk ? 1 : 0;
         // descending: larger key first
         return kKeys - 1 - (split * kBuckets + degree_bucket(deg));
     };
@@ -94,7 +106,7 @@ ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t ro
         const int64_t deg = P.local_row_ptr[r + 1] - P.local_row_ptr[r];
         if (deg > 0) ++P.nonempty_rows;
         P.max_degree = std::max(P.max_degree, deg);
-        if (deg > kChunkEdges) ++P.n_split_rows;
+        if (deg > P.chunk) ++P.n_split_rows;
         else if (deg >= kWideMin) ++P.n_wide_rows;
         ++count[key_of(r) + 1];
     }
@@ -117,7 +129,7 @@ ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t ro
     for (int64_t i = 0; i < P.n_split_rows; ++i) {
         const int32_t r = P.order[i];
         const int64_t deg = P.local_row_ptr[r + 1] - P.local_row_ptr[r];
-        const int64_t nch = (deg + kChunkEdges - 1) / kChunkEdges;
+        const int64_t nch = (deg + P.chunk - 1) / P.chunk;
         if (slot + nch > INT32_MAX) throw std::invalid_argument("too many chunk slots");
         const int32_t si = static_cast<int32_t>(P.split_rows.size());
         P.split_rows.push_back({r, static_cast<int32_t>(slot), static_cast<int32_t>(nch), 0});
@@ -141,8 +153,8 @@ GroupSchedule build_group_schedule(const ShardPlan& P, int warps, int gpw, int u
     items.reserve(P.chunks.size() + static_cast<size_t>(P.nonempty_rows));
     for (const Int4& c : P.chunks) {
         const int64_t rb = P.local_row_ptr[c.x], re = P.local_row_ptr[c.x + 1];
-        const int64_t e0 = rb + static_cast<int64_t>(c.y) * kChunkEdges;
-        const int64_t n = std::min<int64_t>(kChunkEdges, re - e0);
+        const int64_t e0 = rb + static_cast<int64_t>(c.y) * P.chunk;
+        const int64_t n = std::min<int64_t>(P.chunk, re - e0);
         items.push_back({c.z, static_cast<int32_t>(e0), static_cast<int32_t>(n), c.x + 1});
     }
     for (int64_t i = P.n_split_rows; i < rows; ++i) {

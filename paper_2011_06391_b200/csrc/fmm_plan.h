@@ -14,7 +14,13 @@ namespace fmm {
 // Edges per chunk when a heavy row is split on the reassociating scheme.
 // Chunk boundaries sit at fixed row-relative offsets, so results do not
 // depend on the shard count.
-constexpr int kChunkEdges = 256;
+// Edges per chunk of a split row: a power of two near total_nnz / 8192,
+// clamped to [256, 16384] (measured: config 2 / 3 best at 4096, config 5 at
+// 16384; long single-warp chunks tail small graphs, short ones multiply the
+// partials). A function of the WHOLE graph only, never of a shard, so the
+// chunk boundaries — and the results — do not depend on the shard count.
+// FMM_CHUNK overrides (tuning).
+int choose_chunk_edges(int64_t total_nnz);
 // Unsplit rows at least this long are folded by a whole warp on the fast
 // scheme (a bucket boundary, so they form a prefix of the ordered rows).
 constexpr int kWideMin = 64;
@@ -42,6 +48,7 @@ std::string validate_row_ptr(int64_t m, const int64_t* row_ptr);
 // Work lists for one shard (rows [row_begin, row_end), local row ids).
 struct ShardPlan {
     int64_t row_begin = 0, row_end = 0;   // absolute
+    int chunk = 256;                      // edges per chunk of a split row
     int64_t edge_begin = 0, nnz = 0;      // absolute edge offset, count
     std::vector<int64_t> local_row_ptr;   // rebased, rows+1
     // Rows ordered heavy-first: rows with degree > kChunkEdges first, then by
@@ -61,7 +68,7 @@ struct ShardPlan {
     int64_t max_degree = 0;
 };
 
-ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t row_end);
+ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t row_end, int chunk);
 
 // Per-lane-group work lists for the persistent kernel (fmm_sched.cuh).
 // Items: chunks of split rows {slot, e_begin, n, row+1} and non-empty rows
