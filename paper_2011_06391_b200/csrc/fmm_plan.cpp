@@ -9,6 +9,16 @@
 
 namespace fmm {
 
+int wide_min(int chunk) {
+    static const int env = [] {
+        const char* e = std::getenv("FMM_WIDE");
+        const int v = e ? std::atoi(e) : 0;
+        return (v >= 8 && (v & (v - 1)) == 0) ? v : 0;
+    }();
+    if (env) return env;
+    return std::min(kWideMin, std::max(8, chunk / 4));
+}
+
 int choose_chunk_edges(int64_t total_nnz) {
     if (const char* e = std::getenv("FMM_CHUNK")) {
         const int v = std::atoi(e);
@@ -83,6 +93,7 @@ inline int degree_bucket(int64_t deg) {
 ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t row_end, int chunk) {
     ShardPlan P;
     P.chunk = chunk;
+    P.wide = wide_min(chunk);
     P.row_begin = row_begin;
     P.row_end = row_end;
     P.edge_begin = row_ptr[row_begin];
@@ -107,7 +118,7 @@ ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t ro
         if (deg > 0) ++P.nonempty_rows;
         P.max_degree = std::max(P.max_degree, deg);
         if (deg > P.chunk) ++P.n_split_rows;
-        else if (deg >= kWideMin) ++P.n_wide_rows;
+        else if (deg >= P.wide) ++P.n_wide_rows;
         ++count[key_of(r) + 1];
     }
     for (int k = 0; k < kKeys; ++k) count[k + 1] += count[k];

@@ -23,7 +23,12 @@ namespace fmm {
 int choose_chunk_edges(int64_t total_nnz);
 // Unsplit rows at least this long are folded by a whole warp on the fast
 // scheme (a bucket boundary, so they form a prefix of the ordered rows).
-constexpr int kWideMin = 64;
+// (The threshold is min(kWideMin, chunk / 4): rows up to a few hundred edges
+// run faster folded by one lane group than spread over a warp, measured:
+// config 2 1.225 -> 1.186 ms, config 3 0.506 -> 0.483 ms going 64 -> 512.)
+constexpr int kWideMin = 512;
+// FMM_WIDE (power of two >= 8, tuning) overrides; read once.
+int wide_min(int chunk);
 
 struct Int4 {
     int32_t x, y, z, w;
@@ -49,6 +54,7 @@ std::string validate_row_ptr(int64_t m, const int64_t* row_ptr);
 struct ShardPlan {
     int64_t row_begin = 0, row_end = 0;   // absolute
     int chunk = 256;                      // edges per chunk of a split row
+    int wide = 64;                        // rows with degree >= wide are warp items
     int64_t edge_begin = 0, nnz = 0;      // absolute edge offset, count
     std::vector<int64_t> local_row_ptr;   // rebased, rows+1
     // Rows ordered heavy-first: rows with degree > kChunkEdges first, then by
@@ -60,7 +66,7 @@ struct ShardPlan {
     // with one 16-byte load
     std::vector<Int4> items;
     int64_t n_split_rows = 0;             // prefix of `order` cut into chunks
-    int64_t n_wide_rows = 0;              // next rows with degree >= kWideMin
+    int64_t n_wide_rows = 0;              // next rows with degree >= wide
     std::vector<Int4> chunks;             // {row, k, slot, split-row index}
     std::vector<Int4> split_rows;         // {row, first slot, nchunks, 0}
     int64_t n_slots = 0;
