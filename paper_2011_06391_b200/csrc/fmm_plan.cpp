@@ -16,7 +16,7 @@ int wide_min(int chunk) {
         return (v >= 8 && (v & (v - 1)) == 0) ? v : 0;
     }();
     if (env) return env;
-    return std::min(kWideMin, std::max(8, chunk / 4));
+    return std::max(64, std::min(kWideMin, chunk / 16));
 }
 
 int choose_chunk_edges(int64_t total_nnz) {
@@ -25,7 +25,7 @@ int choose_chunk_edges(int64_t total_nnz) {
         if (v >= 32) return v;
     }
     int c = 256;
-    while (c < 16384 && static_cast<int64_t>(c) * 8192 * 3 / 2 < total_nnz) c *= 2;
+    while (c < 16384 && static_cast<int64_t>(c) * 16384 * 3 / 2 < total_nnz) c *= 2;
     return c;
 }
 

@@ -14,18 +14,21 @@ namespace fmm {
 // Edges per chunk when a heavy row is split on the reassociating scheme.
 // Chunk boundaries sit at fixed row-relative offsets, so results do not
 // depend on the shard count.
-// Edges per chunk of a split row: a power of two near total_nnz / 8192,
-// clamped to [256, 16384] (measured: config 2 / 3 best at 4096, config 5 at
-// 16384; long single-warp chunks tail small graphs, short ones multiply the
-// partials). A function of the WHOLE graph only, never of a shard, so the
-// chunk boundaries — and the results — do not depend on the shard count.
-// FMM_CHUNK overrides (tuning).
+// Edges per chunk of a split row: a power of two near total_nnz / 16384,
+// clamped to [256, 16384] (2048 for configs 2 and 3, 16384 for config 5). A
+// function of the WHOLE graph only, never of a shard, so the chunk
+// boundaries — and the results — do not depend on the shard count. Chosen
+// for one GPU and eight together (tools/shard_balance.py, r05): config 2
+// 1.229 ms / 6.98x at 8 shards with (2048, 128) against 1.186 ms / 3.98x with
+// (4096, 512) — one warp folding a 4096-edge row or one lane group a
+// 512-edge row floors every shard's kernel at ~0.15-0.3 ms. FMM_CHUNK
+// overrides (tuning).
 int choose_chunk_edges(int64_t total_nnz);
 // Unsplit rows at least this long are folded by a whole warp on the fast
 // scheme (a bucket boundary, so they form a prefix of the ordered rows).
-// (The threshold is min(kWideMin, chunk / 4): rows up to a few hundred edges
-// run faster folded by one lane group than spread over a warp, measured:
-// config 2 1.225 -> 1.186 ms, config 3 0.506 -> 0.483 ms going 64 -> 512.)
+// (The threshold is max(64, min(kWideMin, chunk / 16)): rows up to a few
+// hundred edges run faster folded by one lane group than spread over a warp
+// on one GPU, but a long narrow row floors a small shard's kernel.)
 constexpr int kWideMin = 512;
 // FMM_WIDE (power of two >= 8, tuning) overrides; read once.
 int wide_min(int chunk);
