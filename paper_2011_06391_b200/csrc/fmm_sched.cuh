@@ -13,7 +13,7 @@
 // only its own 16-byte pieces of every row, so no cross-lane shared-memory
 // synchronisation is needed (cp.async.wait_group per thread suffices).
 //
-// Items are whole rows (degree <= kChunkEdges) or fixed 256-edge chunks of
+// Items are whole rows (degree <= the plan's chunk size) or fixed-size chunks of
 // heavy rows, assigned to lane groups longest-first by the host
 // (fmm_plan.cpp build_group_schedule); per item the group folds its edges in
 // storage order exactly like update_u (kernel.hpp:92-106). Empty rows are
