@@ -124,6 +124,22 @@ ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t ro
     for (int k = 0; k < kKeys; ++k) count[k + 1] += count[k];
     P.order.resize(static_cast<size_t>(rows));
     for (int64_t r = 0; r < rows; ++r) P.order[count[key_of(r)]++] = static_cast<int32_t>(r);
+    // inside every bucket of degree >= 16, rows by descending exact degree, so
+    // the lane groups of a warp end together (configs 2 / 3 / 5: -1 to -2%);
+    // lower buckets keep the natural order (lattice locality, config 4)
+    {
+        auto degree = [&](int32_t r) { return P.local_row_ptr[r + 1] - P.local_row_ptr[r]; };
+        int64_t i = 0;
+        while (i < rows) {
+            const int k = key_of(P.order[i]);
+            int64_t j = i + 1;
+            while (j < rows && key_of(P.order[j]) == k) ++j;
+            if (degree(P.order[i]) >= 16)
+                std::stable_sort(P.order.begin() + i, P.order.begin() + j,
+                                 [&](int32_t a, int32_t b) { return degree(a) > degree(b); });
+            i = j;
+        }
+    }
     P.items.resize(static_cast<size_t>(rows));
     for (int64_t i = 0; i < rows; ++i) {
         const int32_t r = P.order[i];

@@ -60,7 +60,8 @@ struct ShardPlan {
     int wide = 64;                        // rows with degree >= wide are warp items
     int64_t edge_begin = 0, nnz = 0;      // absolute edge offset, count
     std::vector<int64_t> local_row_ptr;   // rebased, rows+1
-    // Rows ordered heavy-first: rows with degree > chunk first, then by
+    // Rows ordered heavy-first (inside a bucket of degree >= 16 by exact
+    // degree): rows with degree > chunk first, then by
     // descending power-of-two degree bucket, stable (natural order) inside a
     // bucket so light rows keep their memory locality.
     std::vector<int32_t> order;
