@@ -44,6 +44,10 @@ inline bool launch_aligned32(const KParams& p, const Ops& ops, int d, int varian
                 if (variant == 21) { launch_one<Ops, 4, 8, 4, 4, EXACT, false>(p, ops, s); return true; }
                 if (variant == 22) { launch_one<Ops, 16, 8, 1, 4, EXACT, false>(p, ops, s); return true; }
                 if (variant == 23) { launch_one<Ops, 8, 8, 2, 2, EXACT, false>(p, ops, s); return true; }
+                if (variant == 24) { launch_one<Ops, 8, 8, 2, 4, EXACT, false, 3>(p, ops, s); return true; }
+                if (variant == 25) { launch_one<Ops, 8, 8, 2, 2, EXACT, false, 3>(p, ops, s); return true; }
+                if (variant == 26) { launch_one<Ops, 16, 8, 1, 4, EXACT, false, 3>(p, ops, s); return true; }
+                if (variant == 27) { launch_one<Ops, 16, 8, 1, 2, EXACT, false, 4>(p, ops, s); return true; }
                 launch_one<Ops, 8, 8, 2, 4, EXACT, false>(p, ops, s); return true;  // config 2
             }
             launch_one<Ops, 8, 8, 2, 2, EXACT, false>(p, ops, s); return true;
