@@ -741,8 +741,16 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
                 cnext[q] = 0;
                 anext[q] = 1.0f;
                 if (eb < n) {
-                    cnext[q] = ld_stream_i32(p.col + e0 + eb);
-                    if (has_val) anext[q] = ld_stream_f32(p.val + e0 + eb);
+                    if constexpr (KPL > 1) {
+                        // KPL loads per lane into the same row's indices, the
+                        // lanes' rows apart: keep those sectors in L1 so the
+                        // batch fetches them from L2 once, not KPL times
+                        cnext[q] = __ldg(p.col + e0 + eb);
+                        if (has_val) anext[q] = __ldg(p.val + e0 + eb);
+                    } else {
+                        cnext[q] = ld_stream_i32(p.col + e0 + eb);
+                        if (has_val) anext[q] = ld_stream_f32(p.val + e0 + eb);
+                    }
                 }
             }
         };
