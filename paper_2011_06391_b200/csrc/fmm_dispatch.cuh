@@ -75,7 +75,12 @@ inline bool launch_aligned(const KParams& p, const Ops& ops, int d, int variant,
             if (variant == 2) { launch_one<Ops, 1, 2, 1, 16, EXACT, false>(p, ops, s); return true; }
             if (variant == 6) { launch_one<Ops, 1, 2, 1, 8, EXACT, false, 6>(p, ops, s); return true; }
             if (variant == 0) { launch_one<Ops, 1, 2, 1, 8, EXACT, false>(p, ops, s); return true; }
-            launch_one<Ops, 1, 2, 1, 4, EXACT, false, 8>(p, ops, s); return true;  // config 4
+            if (variant == 3) { launch_one<Ops, 1, 2, 1, 2, EXACT, false, 8>(p, ops, s); return true; }
+            if (variant == 4) { launch_one<Ops, 1, 2, 1, 8, EXACT, false, 8>(p, ops, s); return true; }
+            if (variant == 5) { launch_one<Ops, 1, 2, 1, 4, EXACT, false, 8>(p, ops, s); return true; }
+            // config 4: with the index slots read through L1 the register cap
+            // of 8 blocks/SM no longer pays (0.0963 vs 0.0983 ms, r08f)
+            launch_one<Ops, 1, 2, 1, 4, EXACT, false>(p, ops, s); return true;
         case 4: launch_one<Ops, 1, 4, 1, 8, EXACT, false>(p, ops, s); return true;
         case 8: launch_one<Ops, 2, 4, 1, 8, EXACT, false>(p, ops, s); return true;
         case 16: launch_one<Ops, 4, 4, 1, 8, EXACT, false>(p, ops, s); return true;
