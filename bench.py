@@ -4,18 +4,30 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
 Workload: BASELINE.json configs[1] (config 2: sigmoid graph embedding, R-MAT
-scale 20, ef 16, d=128), one fused call per step. Metric: nnz*d/s (whole job)
-with the achieved HBM roofline fraction of the fused kernel alongside.
+scale 20, ef 16, d=128) by default; --config 3 / 5 select the iterative
+workloads. Metric: nnz*d/s (whole job).
 
-ours:      inputs resident in HBM, kernel timed with CUDA events on the launch
-           stream, L2 flushed (256 MiB write) between timed steps outside the
-           events; rows split across ranks by part1d balanced on nnz plus a
-           per-row cost (fmm_part1d_weighted; strong scaling:
-           the graph is fixed, each rank computes its row block).
-           e2e: the same call through the C ABI with pinned HOST buffers
-           (X host->device, Z device->host inside the timed region).
+ours:      one step = one fused call over every rank's row block (part1d
+           balanced on nnz plus a per-row cost; rows never split) with the
+           inputs resident in HBM; with N > 1 the step also carries the Z
+           exchange of an iterative epoch: every finished z row is stored by
+           the kernel itself, over NVLink (CUDA IPC), into the next-iterate
+           buffer of each peer that reads it (halo masks), and a
+           stream-ordered barrier closes the step. X is held fixed across
+           steps, so every step moves the same bytes (an X <- Z feedback would
+           move exactly these). Device time: CUDA events on the launch stream,
+           max over ranks; L2 flushed (256 MiB write) between timed steps
+           outside the events. e2e: the same call through the C ABI with
+           pinned HOST buffers (X host->device, Z device->host in the timed
+           region). roofline: the row kernel's DRAM bytes per launch from the
+           committed `ncu --set full` capture over the live launch time,
+           against MEASURED_PEAKS.json; B_alg (every gather charged once)
+           and the L2->SM delivery are reported beside it.
 reference: the unmodified reference fusedmm::fused_mm<float> (oracle/_ref,
-           compiled from /root/reference) on the host cores, all threads.
+           compiled from /root/reference) on all host cores, its inputs built
+           by the reference's own generator (oracle.ref_workload: rmat_generate
+           + the BASELINE recipe; bitwise equal to ours, tests/test_oracle.py)
+           — no library of this repo is loaded on that arm.
 """
 from __future__ import annotations
 
@@ -37,10 +49,10 @@ PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM_GBS = 6650.0
 
 
-def ncu_traffic(cfg: int):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the row
-    kernel for this config, from the newest committed `ncu --set full`
-    capture (profiles/<tag>_summary.json), or (None, why)."""
+def ncu_capture(cfg: int):
+    """(report dict, source) of the newest committed `ncu --set full` capture
+    of this config's row kernel (profiles/<tag>_summary.json), or (None, why).
+    Per launch: dram__bytes_read.sum + dram__bytes_write.sum, duration, L2->SM."""
     for path in sorted((ROOT / "profiles").glob("r*_summary.json"), reverse=True):
         try:
             s = json.loads(path.read_text())
@@ -48,36 +60,8 @@ def ncu_traffic(cfg: int):
             continue
         for name, rep in s.get("reports", {}).items():
             if name.endswith(f"config{cfg}_rows") and "dram_bytes_total" in rep:
-                return rep["dram_bytes_total"], f"{path.name}:{name} (ncu --set full, one launch)"
+                return rep, f"{path.name}:{name} (ncu --set full, one launch)"
     return None, "no committed ncu capture for this config"
-
-
-def l2_delivery(cfg: int):
-    """(L2->SM bytes per launch of the row kernel from the newest committed
-    ncu capture, the measured delivery ceiling of config 2's own gather
-    stream (tools/gather_pattern.py: plain row gathers of the real CSR column
-    stream, best shape), source) or Nones."""
-    got, src = None, None
-    for path in sorted((ROOT / "profiles").glob("r*_summary.json"), reverse=True):
-        try:
-            s = json.loads(path.read_text())
-        except Exception:
-            continue
-        for name, rep in s.get("reports", {}).items():
-            if name.endswith(f"config{cfg}_rows") and "l1tex__m_xbar2l1tex_read_bytes.sum" in rep:
-                got, src = rep["l1tex__m_xbar2l1tex_read_bytes.sum"], f"{path.name}:{name}"
-                break
-        if got is not None:
-            break
-    ceiling = None
-    if cfg == 2:
-        for path in sorted((ROOT / "profiles").glob("r*_gather_pattern.log"), reverse=True):
-            vals = [float(l.split()[-2]) for l in path.read_text().splitlines()
-                    if (l.startswith("/tmp/g_csr.bin") or l.startswith("/tmp/g2_csr.bin")) and l.endswith("TB/s")]
-            if vals:
-                ceiling = (max(vals) * 1e3, path.name)
-                break
-    return got, src, ceiling
 
 
 def hbm_peak():
@@ -145,6 +129,12 @@ def load_workload(cfg: int):
     return w, time.time() - t0
 
 
+def config_dict(w) -> dict:
+    """The `config` object of the JSON line: identical on both arms."""
+    return {"workload": w.name, "desc": w.description, "rows": int(w.A.nrows), "nnz": int(w.A.nnz()),
+            "d": int(w.d)}
+
+
 # Workloads above this many edges are timed on the CPU through a row sample
 # (config 5: ~1e9 edges, ~50-100 s per reference call).
 CPU_SAMPLE_NNZ = 64_000_000
@@ -152,8 +142,9 @@ CPU_SAMPLE_NNZ = 64_000_000
 
 def cpu_sample(w, max_nnz: int = CPU_SAMPLE_NNZ):
     """(A_s, X_s, Y, description): the whole workload, or a seeded random
-    subset of rows with about max_nnz edges (all columns kept, Y = full X)."""
-    from paper_2011_06391_b200 import fusedmm as F
+    subset of rows with about max_nnz edges (all columns kept, Y = full X).
+    Plain oracle containers only (the reference arm loads no repo library)."""
+    import oracle
     A, X = w.A, w.X
     if A.nnz() <= max_nnz:
         return A, X, X, f"full {w.name} fused_mm call"
@@ -164,8 +155,9 @@ def cpu_sample(w, max_nnz: int = CPU_SAMPLE_NNZ):
     rp = np.concatenate([[0], np.cumsum(deg[take])]).astype(np.int64)
     idx = np.concatenate([np.arange(A.row_ptr[r], A.row_ptr[r + 1]) for r in take]) if take.size else \
         np.zeros(0, np.int64)
-    As = F.CsrMatrix(int(take.size), A.ncols, rp, A.col_idx[idx], None if A.unit_values else A.values[idx])
-    Xs = F.DenseMatrix.wrap(X.array[take])
+    unit = bool(getattr(A, "unit_values", False))
+    As = oracle._Csr(int(take.size), A.ncols, rp, A.col_idx[idx], None if unit else A.values[idx])
+    Xs = oracle._Dense(np.ascontiguousarray(X.array[take]))
     return As, Xs, X, (f"{take.size} random rows of {w.name} ({As.nnz()} of {A.nnz()} edges), "
                        f"Y = full X")
 
@@ -202,10 +194,21 @@ def cpu_reference_run(w, steps: int, warmup: int, budget_s: float | None):
 
 
 def run_reference(args):
+    """The reference's own CPU implementation on this box's host cores, on
+    the same workload as ours (inputs from the reference generator when
+    oracle/_ref is built: no library of this repo is loaded)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    w, _ = load_workload(args.config)
+    import oracle
+    t0 = time.time()
+    if oracle.ref_available() and args.config in (2, 3, 5):
+        w = oracle.ref_workload(args.config)
+        inputs = "reference generator (oracle/_ref: rmat_generate + BASELINE recipe)"
+    else:
+        w, _ = load_workload(args.config)
+        inputs = "repo host generator (libfmm_gen)"
+    gen_s = time.time() - t0
     kind, threads, times, nnzd, sample = cpu_reference_run(w, args.steps, args.warmup, None)
     sec = sum(times) / len(times)
     value = nnzd / sec
@@ -214,8 +217,8 @@ def run_reference(args):
         "n_gpus": world, "steps": len(times), "warmup": args.warmup,
         "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE.json recipe)",
-        "config": {"workload": w.name, "desc": w.description, "nnz": w.A.nnz(), "d": w.d,
-                   "rows": w.A.nrows},
+        "config": config_dict(w),
+        "details": {"inputs": inputs, "gen_seconds": round(gen_s, 2)},
         "cpu_baseline": {"value": value, "unit": "nnz*d/s", "cores": threads, "kind": kind,
                          "sample": f"{sample} per step ({len(times)} steps)"},
         "e2e": {"value": value, "unit": "nnz*d/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -230,6 +233,7 @@ def run_ours(args):
 
     from paper_2011_06391_b200 import fusedmm as F
     from paper_2011_06391_b200 import _lib
+    from paper_2011_06391_b200.shard import ShardedFusedMM
 
     rank, world, local = dist_env()
     # FMM_BENCH_SHARE_GPU=1 (testing only): every rank on GPU 0 with gloo, to
@@ -248,28 +252,52 @@ def run_ours(args):
     w, gen_s = load_workload(args.config)
     A, X, spec, d = w.A, w.X, w.spec, w.d
     m = A.nrows
-    plan = F.shard_bounds(A, world, d)  # part1d balanced on nnz + per-row cost
-    rb, re = plan.boundaries[rank], plan.boundaries[rank + 1]
-
-    ctx = F.Context([dev.index])
     stream = torch.cuda.Stream(dev)  # the lib launches here; events are recorded here
     torch.cuda.set_stream(stream)
-    ctx.set_stream(0, stream.cuda_stream)
-    g = F.DeviceGraph(ctx, A, rb, re)
+
+    # one rank's share: rows [rb, re) of the cost-balanced part1d partition
+    sh = ShardedFusedMM(A, d, spec, device=dev, exchange="fused")
+    sh.ctx.set_stream(0, stream.cuda_stream)
+    rb, re = sh.rb, sh.re
+    g = sh.graph
     info = g.info()
 
     X_dev = torch.from_numpy(X.array).to(dev)
-    Z_dev = torch.empty((re - rb, d), dtype=torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     st = _lib.fmm_stats()
+    exchange = None
+    if world > 1:
+        # the epoch's Z exchange, fused into the kernel: z rows go straight
+        # into each reading peer's next-iterate buffer (halo masks)
+        sh.set_halo_masks()
+        nxt = torch.empty_like(X_dev)
+        peers = sh.map_peer_buffers([nxt])
+        peer_next = [peers[q][0] for q in sorted(peers)]
 
-    def step():
-        g.run_device(X_dev.data_ptr(), m, X_dev.data_ptr(), Z_dev.data_ptr(), d, spec, stats=st)
+        def step():
+            sh.step_exchange(X_dev, nxt, peer_next)
+        sent = torch.tensor([sh.exchange_rows * d * 4, sh.exchange_rows_all * d * 4], dtype=torch.float64,
+                            device=dev)
+        tot = sent.clone()
+        dist.all_reduce(tot)
+        mx = sent.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        exchange = {"how": "in-kernel P2P stores (CUDA IPC over NVLink) of each z row into the next-iterate "
+                           "buffer of every peer that reads it, then a stream-ordered NCCL barrier",
+                    "bytes_per_step_total": int(tot[0].item()), "bytes_per_step_max_rank": int(mx[0].item()),
+                    "bytes_per_step_without_halo_masks": int(tot[1].item()),
+                    "cut_by_masks": 1.0 - float(tot[0].item()) / max(float(tot[1].item()), 1.0)}
+    else:
+        Z_dev = torch.empty((re - rb, d), dtype=torch.float32, device=dev)
 
+        def step():
+            g.run_device(X_dev.data_ptr(), m, X_dev.data_ptr(), Z_dev.data_ptr(), d, spec, stats=st)
+
+    launches0 = sh.launches
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    launches_per_step = int(st.launches)
+    launches_per_step = (sh.launches - launches0) // max(args.warmup, 1) if world > 1 else int(st.launches)
 
     # ---- timed region: K steps, L2 flushed between steps outside the events
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -300,26 +328,43 @@ def run_ours(args):
 
     nnzd_total = A.nnz() * d
     value = nnzd_total * args.steps / (t_max_ms / 1e3)
+    mean_ms = kernel_ms_total / args.steps
 
-    # roofline of this rank's fused kernels: algorithmic bytes per launch
+    # ---- roofline of the row kernel: DRAM bytes per launch (committed ncu
+    # capture of the same kernel on the whole graph) over the live launch time
     nnz_r = int(A.row_ptr[re] - A.row_ptr[rb])
     rows_r = re - rb
     deg = np.diff(A.row_ptr[rb:re + 1])
-    alg = (8 * (rows_r + 1) + 4 * nnz_r + 4 * d * nnz_r + 4 * d * rows_r
-           + (4 * nnz_r if w.weighted else 0) + (4 * d * int(np.count_nonzero(deg)) if spec.vop != 2 else 0))
-    mean_ms = kernel_ms_total / args.steps
-    achieved = alg / (mean_ms / 1e3) / 1e9
+    # compulsory (each array once): row_ptr, columns, values, X, Z
+    compulsory = (8 * (rows_r + 1) + 4 * nnz_r + (4 * nnz_r if w.weighted else 0)
+                  + 4 * d * A.ncols + 4 * d * rows_r)
+    b_alg = (8 * (rows_r + 1) + 4 * nnz_r + 4 * d * nnz_r + 4 * d * rows_r
+             + (4 * nnz_r if w.weighted else 0) + (4 * d * int(np.count_nonzero(deg)) if spec.vop != 2 else 0))
     peak, peak_src = hbm_peak()
-    l2_bytes, l2_src, l2_ceiling = l2_delivery(args.config)
-    delivery = None
-    if l2_bytes is not None:
-        ach = l2_bytes * (nnz_r / max(A.nnz(), 1)) / (mean_ms / 1e3) / 1e9
-        delivery = {"what": "L2->SM bytes of the row kernel (ncu l1tex__m_xbar2l1tex_read_bytes) per launch time",
-                    "achieved": ach, "unit": "GB/s", "bytes_source": l2_src,
-                    "ceiling": l2_ceiling[0] if l2_ceiling else None,
-                    "frac": ach / l2_ceiling[0] if l2_ceiling else None,
-                    "ceiling_source": (f"{l2_ceiling[1]}: plain row gathers of this config's CSR column "
-                                       "stream, best load width / occupancy") if l2_ceiling else None}
+    cap, cap_src = ncu_capture(args.config)
+    roofline = {"bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_src,
+                "kernel": "fmm_rows_kernel (split-row chunks folded in-kernel)"}
+    if cap is not None and world == 1:
+        traffic = float(cap["dram_bytes_total"])
+        achieved = traffic / (mean_ms / 1e3) / 1e9
+        roofline.update({
+            "achieved": achieved, "frac": achieved / peak, "traffic": traffic, "traffic_source": cap_src,
+            "what": "achieved = ncu DRAM bytes (read + write) per launch / live mean launch time",
+            "ncu_kernel": cap.get("kernel"), "ncu_launch_ms": 1e3 * float(cap["gpu__time_duration.sum"]),
+            "ncu_dram_throughput_pct": cap.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")})
+        l2b = cap.get("l1tex__m_xbar2l1tex_read_bytes.sum")
+        if l2b is not None:
+            roofline["l2_to_sm"] = {"bytes_per_launch": float(l2b),
+                                    "achieved_gbs": float(l2b) / (mean_ms / 1e3) / 1e9,
+                                    "what": "L2->SM bytes (ncu l1tex__m_xbar2l1tex_read_bytes) / launch time"}
+    else:
+        roofline.update({"achieved": None, "frac": None, "traffic": None,
+                         "traffic_source": cap_src if cap is None else "per-rank shard: whole-graph capture n/a"})
+    roofline["compulsory_bytes"] = compulsory
+    roofline["compulsory_frac"] = compulsory / (mean_ms / 1e3) / 1e9 / peak
+    roofline["gather_bytes"] = b_alg
+    roofline["gather_bytes_what"] = ("B_alg of SURVEY.md 8(d): every y_v gather charged once (most are "
+                                     "served by L2, so B_alg/t is not an HBM rate)")
 
     # ---- e2e through the C ABI with pinned host buffers
     Xh = F.PinnedBuffer(X.array.shape)  # fmm_host_alloc: page-locked
@@ -357,23 +402,28 @@ def run_ours(args):
         cpu = {"value": nnzd_s / sec, "unit": "nnz*d/s", "cores": threads, "kind": kind,
                "sample": f"{sample} x{len(times)} (1 warm-up), all host threads"}
 
+    if world > 1:
+        sh.unmap_peer_buffers()
+    g_e.free()
+    ctx_e.close()
+    sh.close()
+    Xh.close()
+    Zh.close()
     if rank == 0:
         line = {
             "metric": "nnz*d/s", "value": value, "unit": "nnz*d/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded, BASELINE.json recipe)",
-            "config": {"workload": w.name, "desc": w.description, "rows": m, "nnz": A.nnz(), "d": d,
-                       "parallelism": f"row-shard x{world} (part1d, nnz + per-row cost)",
-                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                       "split_rows": int(info.split_rows), "max_degree": int(info.max_degree),
-                       "gen_seconds": round(gen_s, 2)},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(args.config)[0],
-                         "traffic_source": ncu_traffic(args.config)[1],
-                         "alg_bytes_per_launch": alg, "peak_source": peak_src,
-                         "kernel": "fmm_rows_kernel (split-row chunks folded in-kernel)",
-                         "l2_to_sm": delivery},
+            "config": config_dict(w),
+            "details": {"parallelism": f"row-shard x{world} (part1d, nnz + per-row cost)",
+                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                        "split_rows": int(info.split_rows), "max_degree": int(info.max_degree),
+                        "gen_seconds": round(gen_s, 2),
+                        "step": ("fused call + halo exchange of the epoch's Z (X fixed across steps)"
+                                 if world > 1 else "one fused call")},
+            "exchange": exchange,
+            "roofline": roofline,
             "e2e": {"value": e2e_value, "unit": "nnz*d/s", "h2d_bytes_per_step": int(m * d * 4),
                     "d2h_bytes_per_step": int(rows_r * d * 4), "steps": e2e_steps,
                     "how": "fmm_run(FMM_HOST_PTRS|FMM_ASYNC) pinned host X in / Z out every step, fmm_sync",

@@ -103,9 +103,13 @@ enum {
                                   fmm_sync                                  */
     FMM_EXACT = 1u << 2,       /* force bit-exact scheme    */
     FMM_FAST = 1u << 3,        /* force reassociating scheme (FMA, splits)  */
-    FMM_EXCHANGE_COPIES = 1u << 4 /* fmm_iterate: exchange Z slices with
+    FMM_EXCHANGE_COPIES = 1u << 4, /* fmm_iterate: exchange Z slices with
                                   peer copies after the kernels instead of
                                   the fused P2P-store epilogue (default)    */
+    FMM_PEERS_ALL = 1u << 5    /* fmm_run_peers / fmm_iterate: store every
+                                  row to every peer, ignoring the halo mask
+                                  (e.g. the last iteration, when the caller
+                                  wants the iterate fully replicated)       */
 };
 
 /* Mirrors KernelStats (kernel.hpp:51-55) plus device-side evidence. */
@@ -131,6 +135,11 @@ typedef struct fmm_graph_info {
     int64_t split_chunks;
     int32_t shards;
     int32_t has_values;
+    /* Halo exchange (iterative workloads): rows stored to peers per
+     * exchange with the per-row peer masks (sum over shards of popcount),
+     * and without them (every row to every peer). 0 / 0 before masks exist. */
+    int64_t exchange_rows;
+    int64_t exchange_rows_all;
 } fmm_graph_info;
 
 typedef struct fmm_ctx fmm_ctx;
@@ -187,6 +196,15 @@ fmm_status fmm_graph_upload(fmm_ctx* ctx, int64_t m, int64_t n,
                             const float* values, int64_t row_begin,
                             int64_t row_end, fmm_graph** out);
 fmm_status fmm_graph_free(fmm_graph* g);
+/* Replace the edge values a_uv of an uploaded graph in place (values: the
+ * full host array of the m-row CSR the graph was uploaded from, NULL = all
+ * ones); the structure is kept. For callers that change A.values between
+ * calls (the reference reads A afresh on every fused_mm). */
+fmm_status fmm_graph_update_values(fmm_graph* g, const float* values);
+/* 64-bit content fingerprint of a host buffer (multi-threaded, ~memory
+ * bandwidth): the wrappers key their uploaded-graph caches on the contents
+ * of row_ptr / col_idx / values, not on their addresses. */
+uint64_t fmm_fingerprint(const void* data, size_t bytes);
 fmm_status fmm_graph_get_info(const fmm_graph* g, fmm_graph_info* out);
 /* Boundaries of the shards (length shards+1, absolute row ids). */
 fmm_status fmm_graph_shard_bounds(const fmm_graph* g, int64_t* bounds);
@@ -236,6 +254,18 @@ fmm_status fmm_run_peers(fmm_ctx* ctx, const fmm_graph* g,
                          int64_t ny, const float* Y, float* Z,
                          float* const* peers, int npeer, uint32_t flags,
                          fmm_stats* stats);
+
+/* Halo masks for the one-process-per-GPU exchange. need[c] (n bytes) is
+ * set to 1 for every column c some edge of g points at (0 elsewhere): the
+ * rows this graph's shard READS. A rank gathers every peer's need array and
+ * passes mask[r] (row_end-row_begin bytes, bit q = peer slot q reads row
+ * row_begin+r; slots in the order of fmm_run_peers' peers array) to
+ * fmm_graph_set_peer_mask; fmm_run_peers then stores row r only to the
+ * peers whose bit is set (FMM_PEERS_ALL overrides). Results are unchanged:
+ * a peer never reads a row it does not reference. fmm_iterate builds the
+ * same masks for its own shards. */
+fmm_status fmm_graph_column_use(const fmm_graph* g, uint8_t* need);
+fmm_status fmm_graph_set_peer_mask(fmm_graph* g, const uint8_t* mask, int npeer);
 
 #define FMM_IPC_HANDLE_BYTES 64
 /* CUDA IPC: export the allocation dptr lies in (handle: FMM_IPC_HANDLE_BYTES

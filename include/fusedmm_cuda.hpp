@@ -18,6 +18,8 @@
 // the reference's worker threads; the result is bitwise independent of t.
 #pragma once
 
+#include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -102,10 +104,16 @@ inline fmm_opspec fr_attract_ops(float k) {
     return fmm_opspec{FMM_VOP_SUB, FMM_ROP_SQNORM, FMM_SOP_SQK, FMM_MOP_MUL_VOP, FMM_AOP_ASUM, 1.f, k};
 }
 
-// One context per shard count, one uploaded graph cached per context.
+// One context per shard count, one uploaded graph cached per context. The
+// cache is keyed on the CONTENTS of A (fmm_fingerprint of row_ptr, col_idx
+// and values), never on its addresses: the reference reads A afresh on
+// every call (kernel.hpp:297-353), so a CSR rebuilt at the same addresses or
+// edited in place is re-uploaded (values-only changes are re-sent in place).
+// Every call on a context holds its mutex (graph lookup + run), so two host
+// threads sharing a shard count cannot free each other's graph.
 class Context {
 public:
-    explicit Context(int t) {
+    explicit Context(int t) : t_(t) {
         const int ndev = fmm_device_count();
         if (ndev < 1) throw device_error("fusedmm::cuda: no CUDA device (no CPU fallback)");
         std::vector<int> devs(static_cast<size_t>(t));
@@ -126,16 +134,26 @@ public:
         for (auto& c : pool)
             if (c->t_ == t) return *c;
         pool.emplace_back(new Context(t));
-        pool.back()->t_ = t;
         return *pool.back();
     }
 
-    // Upload A unless it is the graph uploaded last (same arrays, same size).
+    // The device copy of A, uploaded (or its values refreshed) when A's
+    // contents differ from the cached graph's. Caller holds mutex().
     template <class Csr>
     fmm_graph* graph_for(const Csr& A) {
-        const void* key[4] = {A.row_ptr.data(), A.col_idx.data(), A.values.data(),
-                              reinterpret_cast<const void*>(static_cast<intptr_t>(A.nnz()))};
-        if (graph_ && std::memcmp(key, key_, sizeof(key)) == 0 && m_ == A.nrows) return graph_;
+        const uint64_t rp = fmm_fingerprint(A.row_ptr.data(), A.row_ptr.size() * sizeof(A.row_ptr[0]));
+        const uint64_t ci = fmm_fingerprint(A.col_idx.data(), A.col_idx.size() * sizeof(A.col_idx[0]));
+        const uint64_t va = fmm_fingerprint(A.values.data(), A.values.size() * sizeof(float));
+        const int64_t shape[3] = {static_cast<int64_t>(A.nrows), static_cast<int64_t>(A.ncols),
+                                  static_cast<int64_t>(A.nnz())};
+        const bool same_structure = graph_ && rp == rp_ && ci == ci_ && std::memcmp(shape, shape_, sizeof(shape)) == 0;
+        if (same_structure) {
+            if (va != va_) {
+                throw_status(fmm_graph_update_values(graph_, A.values.empty() ? nullptr : A.values.data()), ctx_);
+                va_ = va;
+            }
+            return graph_;
+        }
         if (graph_) fmm_graph_free(graph_);
         graph_ = nullptr;
         throw_status(fmm_graph_upload(ctx_, A.nrows, A.ncols, A.row_ptr.data(),
@@ -143,19 +161,28 @@ public:
                                       A.values.empty() ? nullptr : A.values.data(), 0, A.nrows,
                                       &graph_),
                      ctx_);
-        std::memcpy(key_, key, sizeof(key));
-        m_ = A.nrows;
+        rp_ = rp;
+        ci_ = ci;
+        va_ = va;
+        std::memcpy(shape_, shape, sizeof(shape));
         return graph_;
     }
     fmm_ctx* get() const { return ctx_; }
+    std::mutex& mutex() { return mu_; }
 
 private:
     fmm_ctx* ctx_ = nullptr;
     fmm_graph* graph_ = nullptr;
-    const void* key_[4] = {nullptr, nullptr, nullptr, nullptr};
-    int64_t m_ = -1;
+    uint64_t rp_ = 0, ci_ = 0, va_ = 0;
+    int64_t shape_[3] = {-1, -1, -1};
     int t_ = 0;
+    std::mutex mu_;
 };
+
+// KernelOptions::lane_width (kernel.hpp:286-288) on the device: 4 selects
+// the 128-bit-gather shapes (variant 20), 8 and 16 the default 256-bit
+// shapes. tune_lane_width below times them.
+inline int variant_for_lane_width(int w) { return w == 4 ? 20 : -1; }
 
 namespace detail {
 
@@ -179,18 +206,25 @@ fmm_opspec to_c(const Spec& s) {
 }
 
 template <class Csr, class Dense, class Stats>
-Dense run(const Csr& A, const Dense& X, const Dense& Y, const fmm_opspec& c, int t, Stats* stats) {
+Dense run(const Csr& A, const Dense& X, const Dense& Y, const fmm_opspec& c, int t, Stats* stats,
+          int lane_width = 8) {
     check_dims(A, X, Y);
     if (t < 1) throw std::invalid_argument("fused_mm: t must be >= 1");
+    if (lane_width != 4 && lane_width != 8 && lane_width != 16)
+        throw std::invalid_argument("KernelOptions.lane_width must be 4, 8 or 16");
     Dense Z(A.nrows, X.dim);
     fmm_stats st{};
     if (A.nrows > 0) {
         Context& ctx = Context::for_shards(t);
+        std::lock_guard<std::mutex> lk(ctx.mutex());
         fmm_graph* g = ctx.graph_for(A);
         const float* y = (&X == &Y) ? X.data.data() : Y.data.data();
-        throw_status(fmm_run(ctx.get(), g, &c, X.dim, X.data.data(), Y.nrows, y, Z.data.data(),
-                             FMM_HOST_PTRS, &st),
-                     ctx.get());
+        const int prev = fmm_get_variant(ctx.get());
+        fmm_set_variant(ctx.get(), variant_for_lane_width(lane_width));
+        const fmm_status rs = fmm_run(ctx.get(), g, &c, X.dim, X.data.data(), Y.nrows, y, Z.data.data(),
+                                      FMM_HOST_PTRS, &st);
+        fmm_set_variant(ctx.get(), prev);
+        throw_status(rs, ctx.get());
     } else {
         int32_t pat = FMM_PATTERN_GENERIC;
         fmm_pattern_of(&c, &pat);
@@ -220,7 +254,6 @@ template <class Csr, class Dense, class Spec, class Stats = detail::NoStats,
           class Opts = types::KernelOptions>
 Dense fused_mm(const Csr& A, const Dense& X, const Dense& Y, const Spec& spec, int t,
                Stats* stats = nullptr, const Opts& opts = {}) {
-    (void)opts;  // lane_width is a CPU blocking width; the device shape is chosen by d
     const bool user = static_cast<int>(spec.vop) == FMM_VOP_USER ||
                       static_cast<int>(spec.rop) == FMM_ROP_USER ||
                       static_cast<int>(spec.sop) == FMM_SOP_USER ||
@@ -230,7 +263,7 @@ Dense fused_mm(const Csr& A, const Dense& X, const Dense& Y, const Spec& spec, i
         detail::check_dims(A, X, Y);
         throw unsupported("fused_mm: USER slot has no device kernel (use a device op descriptor)");
     }
-    return detail::run(A, X, Y, detail::to_c(spec), t, stats);
+    return detail::run(A, X, Y, detail::to_c(spec), t, stats, opts.lane_width);
 }
 
 // Overload taking the device op descriptor (configs 3/4: tdist_ops(),
@@ -239,6 +272,79 @@ template <class Csr, class Dense, class Stats = detail::NoStats>
 Dense fused_mm(const Csr& A, const Dense& X, const Dense& Y, const fmm_opspec& ops, int t,
                Stats* stats = nullptr) {
     return detail::run(A, X, Y, ops, t, stats);
+}
+
+// update_u (kernel.hpp:81-107): one vertex update, z_u = fold over the
+// stored neighbours (cols, vals) of the five slots, on the device. Spans are
+// any contiguous ranges with data()/size(); scratch is accepted for
+// signature parity (the device keeps x_u and z_u in registers). Runs as a
+// one-row fused call (graph uploaded per call), so it is for single-vertex
+// use, not for loops over every row — fused_mm is.
+template <class ColSpan, class ValSpan, class XSpan, class Dense, class Spec, class ZSpan, class Scratch>
+void update_u(const ColSpan& cols, const ValSpan& vals, const XSpan& x_u, const Dense& Y, const Spec& spec,
+              ZSpan&& z_u, Scratch&& scratch) {
+    (void)scratch;
+    const int64_t d = static_cast<int64_t>(x_u.size());
+    const int64_t k = static_cast<int64_t>(cols.size());
+    if (static_cast<int64_t>(z_u.size()) != d || static_cast<int64_t>(Y.dim) != d)
+        throw std::invalid_argument("update_u: length mismatch");
+    if (static_cast<int64_t>(vals.size()) != k) throw std::invalid_argument("update_u: cols / vals differ in length");
+    types::CsrMatrix A;
+    A.nrows = 1;
+    A.ncols = static_cast<int64_t>(Y.nrows);
+    A.row_ptr = {0, k};
+    A.col_idx.assign(cols.data(), cols.data() + k);
+    A.values.assign(vals.data(), vals.data() + k);
+    types::DenseMatrix X(1, d), Yc(static_cast<int64_t>(Y.nrows), d);
+    std::copy(x_u.data(), x_u.data() + d, X.data.begin());
+    std::copy(Y.data.data(), Y.data.data() + Yc.data.size(), Yc.data.begin());
+    const types::DenseMatrix Z = fused_mm(A, X, Yc, spec, 1);
+    std::copy(Z.data.begin(), Z.data.end(), z_u.data());
+}
+
+// fused_mm_specialized (kernel.hpp:356-378): direct entry to a fast path;
+// GENERIC (or any other value) throws std::invalid_argument as there.
+template <class Pattern, class Csr, class Dense, class T, class Opts = types::KernelOptions>
+Dense fused_mm_specialized(Pattern pattern, const Csr& A, const Dense& X, const Dense& Y, T alpha, int t,
+                           const Opts& opts = {}) {
+    fmm_opspec c{};
+    switch (static_cast<int>(pattern)) {
+        case FMM_PATTERN_SIGMOID_EMBED:
+            c = fmm_opspec{FMM_VOP_MUL, FMM_ROP_RSUM, FMM_SOP_SIGMOID, FMM_MOP_MUL, FMM_AOP_ASUM, 1.f, 1.f};
+            break;
+        case FMM_PATTERN_SPMM_GCN:
+            c = fmm_opspec{FMM_VOP_SEL2ND, FMM_ROP_NOOP, FMM_SOP_NOOP, FMM_MOP_MUL, FMM_AOP_ASUM, 1.f, 1.f};
+            break;
+        case FMM_PATTERN_FR_LAYOUT:
+            c = fmm_opspec{FMM_VOP_ADD, FMM_ROP_NORM, FMM_SOP_SCAL, FMM_MOP_MUL, FMM_AOP_ASUM,
+                           static_cast<float>(alpha), 1.f};
+            break;
+        default:
+            throw std::invalid_argument("fused_mm_specialized: pattern has no fast path");
+    }
+    return detail::run(A, X, Y, c, t, static_cast<detail::NoStats*>(nullptr), opts.lane_width);
+}
+
+// tune_lane_width (kernel.hpp:382-402): times the device shape families the
+// lane widths select (4: 128-bit gathers, 8: the default 256-bit shapes;
+// 16 selects the same shapes as 8) and returns the fastest width.
+template <class Csr, class Dense, class Spec>
+int tune_lane_width(const Csr& A, const Dense& X, const Dense& Y, const Spec& spec, int t, int repeats = 3) {
+    int best_w = 8;
+    double best = 1e300;
+    for (int w : {4, 8}) {
+        types::KernelOptions opts{w};
+        (void)fused_mm(A, X, Y, spec, t, static_cast<detail::NoStats*>(nullptr), opts);  // warm-up
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int r = 0; r < repeats; ++r)
+            (void)fused_mm(A, X, Y, spec, t, static_cast<detail::NoStats*>(nullptr), opts);
+        const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (secs < best) {
+            best = secs;
+            best_w = w;
+        }
+    }
+    return best_w;
 }
 
 // csr_from_coo on the GPU (matrix.hpp:87-140): same signature shape as the

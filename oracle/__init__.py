@@ -91,6 +91,11 @@ def ref_lib() -> C.CDLL:
         L.fmm_ref_read_mm.restype = C.c_int64
         L.fmm_ref_read_mm.argtypes = [C.c_char_p, P64, P64, P64, P64, PF, C.c_int64, C.c_char_p, C.c_int64]
         L.fmm_ref_write_mm.argtypes = [C.c_char_p, C.c_int64, C.c_int64, P64, P64, PF]
+        L.fmm_ref_free.argtypes = [C.c_void_p]
+        L.fmm_ref_rmat_sym.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_uint64,
+                                       C.POINTER(P64), C.POINTER(P64), P64]
+        L.fmm_ref_normal_fill.argtypes = [PF, C.c_int64, C.c_double, C.c_uint64]
+        L.fmm_ref_uniform_fill.argtypes = [PF, C.c_int64, C.c_double, C.c_double, C.c_uint64]
         L.fmm_ref_csr_from_coo.restype = C.c_int64
         L.fmm_ref_csr_from_coo.argtypes = [C.c_int64, C.c_int64, C.c_int64, P64, P64, PF, P64, P64, PF]
         _ref = L
@@ -108,7 +113,11 @@ def _arrs(A, X, Y, f64: bool):
     dt = np.float64 if f64 else np.float32
     Xa = np.ascontiguousarray(X.data if hasattr(X, "data") else X, dtype=dt).reshape(-1)
     Ya = Xa if (Y is X) else np.ascontiguousarray(Y.data if hasattr(Y, "data") else Y, dtype=dt).reshape(-1)
-    V = None if getattr(A, "unit_values", False) else np.ascontiguousarray(A.values, dtype=dt)
+    # the values as they are now (a caller may assign A.values after building
+    # an unweighted matrix); all ones is passed as NULL, which is the same a_uv
+    V = np.ascontiguousarray(A.values, dtype=dt)
+    if V.size == 0 or np.all(V == 1):
+        V = None
     return Xa, Ya, V
 
 
@@ -301,13 +310,117 @@ def oracle_csr_from_coo(rows, cols, vals, m: int, n: int):
 
 def row_errors(Z_gpu: np.ndarray, Z_cpu: np.ndarray) -> np.ndarray:
     """Per-row normwise relative error ||z_gpu - z_cpu|| / ||z_cpu||, rows
-    where both are zero count as 0."""
+    where both are zero count as 0. Non-finite values:
+    elements that agree exactly (the AMAX identity -inf of an empty row, an
+    inf both sides produce) are left out of the norms; a row where the GPU
+    and CPU disagree on which elements are finite, or where either holds a
+    NaN the other does not, is +inf (so it always fails a tolerance check)."""
     a = np.asarray(Z_gpu, np.float64)
     b = np.asarray(Z_cpu, np.float64)
-    num = np.linalg.norm(a - b, axis=1)
-    den = np.linalg.norm(b, axis=1)
+    same = (a == b) | (np.isnan(a) & np.isnan(b))
+    fa, fb = np.isfinite(a), np.isfinite(b)
+    bad = np.any(~same & (~fa | ~fb), axis=1)
+    a0 = np.where(fa & fb, a, 0.0)
+    b0 = np.where(fa & fb, b, 0.0)
+    num = np.linalg.norm(a0 - b0, axis=1)
+    den = np.linalg.norm(b0, axis=1)
     out = np.zeros_like(num)
     nz = den > 0
     out[nz] = num[nz] / den[nz]
     out[(~nz) & (num > 0)] = np.inf
+    out[bad] = np.inf
     return out
+
+
+def ref_rmat_sym(scale: int, edge_factor: int, seed: int, abc=(0.57, 0.19, 0.19)):
+    """BASELINE.json R-MAT recipe from the reference's own rmat_generate
+    (rmat.hpp:24-61) + drop self-loops / symmetrise / sort / unique, as
+    (row_ptr, col). Test infrastructure and the reference arm's inputs."""
+    L = ref_lib()
+    rp, cl, nnz = P64(), P64(), C.c_int64()
+    if L.fmm_ref_rmat_sym(scale, edge_factor, *abc, seed, C.byref(rp), C.byref(cl), C.byref(nnz)) != 0:
+        raise ValueError("rmat_sym: the reference generator threw")
+    n = 1 << scale
+    try:
+        row_ptr = np.ctypeslib.as_array(rp, shape=(n + 1,)).copy()
+        col = np.ctypeslib.as_array(cl, shape=(max(nnz.value, 1),))[:nnz.value].copy()
+    finally:
+        L.fmm_ref_free(C.cast(rp, C.c_void_p))
+        L.fmm_ref_free(C.cast(cl, C.c_void_p))
+    return row_ptr, col
+
+
+def ref_normal_fill(count: int, scale: float, seed: int) -> np.ndarray:
+    out = np.empty(count, np.float32)
+    ref_lib().fmm_ref_normal_fill(out.ctypes.data_as(PF), count, scale, seed)
+    return out
+
+
+def ref_uniform_fill(count: int, lo: float, hi: float, seed: int) -> np.ndarray:
+    out = np.empty(count, np.float32)
+    ref_lib().fmm_ref_uniform_fill(out.ctypes.data_as(PF), count, lo, hi, seed)
+    return out
+
+
+class RefWorkload:
+    """A BASELINE.json workload built without any repo library (reference
+    arm of bench.py): duck-types the fields cpu_reference_run reads."""
+
+    def __init__(self, name, A, X, spec, description):
+        self.name, self.A, self.X, self.spec, self.description = name, A, X, spec, description
+
+    @property
+    def d(self) -> int:
+        return self.X.dim
+
+
+class _Csr:
+    def __init__(self, m, n, row_ptr, col_idx, values=None):
+        self.nrows, self.ncols = m, n
+        self.row_ptr, self.col_idx = row_ptr, col_idx
+        self.values = np.ones(col_idx.size, np.float32) if values is None else values
+        self.unit_values = values is None
+
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1])
+
+
+class _Dense:
+    def __init__(self, arr):
+        self.nrows, self.dim = arr.shape
+        self.data = arr.reshape(-1)
+
+    @property
+    def array(self):
+        return self.data.reshape(self.nrows, self.dim)
+
+
+class _Spec:
+    def __init__(self, vop, rop, sop, mop, aop, alpha=1.0, k=1.0):
+        self.vop, self.rop, self.sop, self.mop, self.aop, self.alpha, self.k = vop, rop, sop, mop, aop, alpha, k
+
+
+# BASELINE.json configs 2, 3 and 5 (SURVEY.md §8(d)) from the reference generator
+_REF_CONFIGS = {
+    2: dict(scale=20, ef=16, d=128, seed=1, x="normal", name="config2_sigmoid",
+            spec=(1, 1, 1, 0, 0), desc="R-MAT scale 20 ef 16 d=128 sigmoid embedding, seed 1"),
+    3: dict(scale=21, ef=8, d=32, seed=2, x="uniform", name="config3_tdist",
+            spec=(3, 16, 16, 16, 0), desc="R-MAT scale 21 ef 8 d=32 t-distribution, 20 iterations, seed 2"),
+    5: dict(scale=24, ef=32, d=256, seed=4, x="normal", name="config5_sigmoid_large",
+            spec=(1, 1, 1, 0, 0), desc="R-MAT scale 24 ef 32 d=256 sigmoid, 5 epochs, seed 4"),
+}
+
+
+def ref_workload(config: int, scale: int | None = None) -> RefWorkload:
+    """Configs 2 / 3 / 5 built by the reference's generator (oracle/_ref)
+    only. `scale` shrinks the R-MAT scale (tests)."""
+    c = _REF_CONFIGS[config]
+    sc = c["scale"] if scale is None else scale
+    rp, cl = ref_rmat_sym(sc, c["ef"], c["seed"])
+    n = 1 << sc
+    if c["x"] == "normal":
+        X = ref_normal_fill(n * c["d"], 0.1, c["seed"])
+    else:
+        X = ref_uniform_fill(n * c["d"], -10.0, 10.0, c["seed"])
+    A = _Csr(n, n, rp, cl)
+    return RefWorkload(c["name"], A, _Dense(X.reshape(n, c["d"])), _Spec(*c["spec"]), c["desc"])

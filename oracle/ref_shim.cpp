@@ -8,7 +8,10 @@
 // Configs 3 and 4 have no reference enum spelling; they run through the
 // reference exactly as SURVEY.md §8(a) prescribes: a USER VOP lambda that
 // emits the whole message vector, ROP=NOOP, SOP=NOOP, MOP=MUL, AOP=ASUM.
+#include <algorithm>
 #include <chrono>
+#include <cstdlib>
+#include <random>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -267,6 +270,93 @@ int fmm_ref_write_mm(const char* path, int64_t m, int64_t n, const int64_t* row_
 
 int fmm_ref_pattern_of(const RefSpec* s) {
     return static_cast<int>(pattern_of(make_ref_spec<float>(*s)));
+}
+
+// ---- reference-arm inputs (bench.py --impl reference): the BASELINE.json
+// workloads built from the reference's OWN generator, so the reference arm
+// maps none of the repo's libraries. Same buffers as the repo's host
+// builder (tests/test_oracle.py pins them bitwise):
+//  * R-MAT graphs: rmat_generate (rmat.hpp:24-61, the unmodified reference)
+//    then the BASELINE recipe — self-loops dropped, both directions, sorted,
+//    deduplicated, unweighted;
+//  * X: blocks of 2^20 values, block b drawn from std::mt19937_64 seeded with
+//    splitmix64(seed + golden*(b+1)); u01 = (r >> 11) * 2^-53; N(0,1) by
+//    Box-Muller on pairs (u1, u2): sqrt(-2 ln(1-u1)) * (cos, sin)(2 pi u2);
+//    U(lo,hi) = lo + (hi-lo)*u01.
+void fmm_ref_free(void* p) { std::free(p); }
+
+int fmm_ref_rmat_sym(int scale, int edge_factor, double a, double b, double c, uint64_t seed, int64_t** row_ptr,
+                     int64_t** col, int64_t* nnz) {
+    try {
+        RmatParams p;
+        p.scale = scale;
+        p.edge_factor = edge_factor;
+        p.a = a;
+        p.b = b;
+        p.c = c;
+        p.d = 1.0 - a - b - c;
+        p.seed = seed;
+        const CsrMatrix<float> G = rmat_generate<float>(p);
+        const int64_t n = G.nrows;
+        std::vector<uint64_t> keys;
+        keys.reserve(static_cast<size_t>(2 * G.nnz()));
+        for (int64_t u = 0; u < n; ++u)
+            for (int64_t e = G.row_ptr[u]; e < G.row_ptr[u + 1]; ++e) {
+                const uint64_t v = static_cast<uint64_t>(G.col_idx[e]);
+                if (v == static_cast<uint64_t>(u)) continue;
+                keys.push_back((static_cast<uint64_t>(u) << scale) | v);
+                keys.push_back((v << scale) | static_cast<uint64_t>(u));
+            }
+        std::sort(keys.begin(), keys.end());
+        keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+        int64_t* rp = static_cast<int64_t*>(std::calloc(static_cast<size_t>(n + 1), sizeof(int64_t)));
+        int64_t* cl = static_cast<int64_t*>(std::malloc(std::max<size_t>(1, keys.size()) * sizeof(int64_t)));
+        const uint64_t mask = (uint64_t(1) << scale) - 1;
+        for (size_t i = 0; i < keys.size(); ++i) {
+            ++rp[(keys[i] >> scale) + 1];
+            cl[i] = static_cast<int64_t>(keys[i] & mask);
+        }
+        for (int64_t r = 0; r < n; ++r) rp[r + 1] += rp[r];
+        *row_ptr = rp;
+        *col = cl;
+        *nnz = static_cast<int64_t>(keys.size());
+        return 0;
+    } catch (...) {
+        return 1;
+    }
+}
+
+static uint64_t ref_block_seed(uint64_t seed, int64_t b) {
+    uint64_t z = seed + 0x9E3779B97F4A7C15ull * static_cast<uint64_t>(b + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+void fmm_ref_normal_fill(float* X, int64_t count, double scale, uint64_t seed) {
+    constexpr int64_t kBlock = int64_t(1) << 20;
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int64_t lo = 0, b = 0; lo < count; lo += kBlock, ++b) {
+        std::mt19937_64 rng(ref_block_seed(seed, b));
+        auto u01 = [&] { return static_cast<double>(rng() >> 11) * 0x1.0p-53; };
+        const int64_t hi = std::min(count, lo + kBlock);
+        for (int64_t i = lo; i < hi; i += 2) {
+            const double u1 = u01(), u2 = u01();
+            const double rad = std::sqrt(-2.0 * std::log(1.0 - u1));
+            X[i] = static_cast<float>(scale * rad * std::cos(two_pi * u2));
+            if (i + 1 < hi) X[i + 1] = static_cast<float>(scale * rad * std::sin(two_pi * u2));
+        }
+    }
+}
+
+void fmm_ref_uniform_fill(float* X, int64_t count, double lo_v, double hi_v, uint64_t seed) {
+    constexpr int64_t kBlock = int64_t(1) << 20;
+    for (int64_t lo = 0, b = 0; lo < count; lo += kBlock, ++b) {
+        std::mt19937_64 rng(ref_block_seed(seed, b));
+        const int64_t hi = std::min(count, lo + kBlock);
+        for (int64_t i = lo; i < hi; ++i)
+            X[i] = static_cast<float>(lo_v + (hi_v - lo_v) * (static_cast<double>(rng() >> 11) * 0x1.0p-53));
+    }
 }
 
 }  // extern "C"

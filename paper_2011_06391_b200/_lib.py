@@ -23,6 +23,7 @@ FMM_ASYNC = 1 << 1
 FMM_EXACT = 1 << 2
 FMM_FAST = 1 << 3
 FMM_EXCHANGE_COPIES = 1 << 4
+FMM_PEERS_ALL = 1 << 5
 
 
 class fmm_opspec(C.Structure):
@@ -42,7 +43,8 @@ class fmm_graph_info(C.Structure):
                 ("row_begin", C.c_int64), ("row_end", C.c_int64),
                 ("nonempty_rows", C.c_int64), ("max_degree", C.c_int64),
                 ("split_rows", C.c_int64), ("split_chunks", C.c_int64),
-                ("shards", C.c_int32), ("has_values", C.c_int32)]
+                ("shards", C.c_int32), ("has_values", C.c_int32),
+                ("exchange_rows", C.c_int64), ("exchange_rows_all", C.c_int64)]
 
 
 # every symbol include/fusedmm_cuda.h declares: name -> (restype, argtypes)
@@ -67,6 +69,10 @@ SIGNATURES = {
     "fmm_graph_upload": (C.c_int, [_P, C.c_int64, C.c_int64, _I64P, _I64P, _FP, C.c_int64,
                                    C.c_int64, C.POINTER(_P)]),
     "fmm_graph_free": (C.c_int, [_P]),
+    "fmm_graph_update_values": (C.c_int, [_P, _FP]),
+    "fmm_fingerprint": (C.c_uint64, [_P, C.c_size_t]),
+    "fmm_graph_column_use": (C.c_int, [_P, _P]),
+    "fmm_graph_set_peer_mask": (C.c_int, [_P, _P, C.c_int]),
     "fmm_graph_get_info": (C.c_int, [_P, C.POINTER(fmm_graph_info)]),
     "fmm_graph_shard_bounds": (C.c_int, [_P, _I64P]),
     "fmm_run": (C.c_int, [_P, _P, C.POINTER(fmm_opspec), C.c_int64, _P, C.c_int64, _P, _P,

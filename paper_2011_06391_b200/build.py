@@ -31,10 +31,12 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xptxas", "-warn-spills", f"-I{INCLUDE}", f"-I{CSRC}"]
+if os.environ.get("FMM_TUNING") == "1":  # tuning variants of the row kernels (tests/sweep_variants.py)
+    NVCC_FLAGS.append("-DFMM_TUNING_VARIANTS")
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-march=x86-64-v3", f"-I{INCLUDE}", f"-I{CSRC}"]
 
 CUDA_SOURCES = ["fmm_api.cu", "fmm_k_sigmoid.cu", "fmm_k_gcn.cu", "fmm_k_fr.cu",
-                "fmm_k_tdist.cu", "fmm_k_frattr.cu", "fmm_k_generic.cu", "fmm_unfused.cu",
+                "fmm_k_tdist.cu", "fmm_k_frattr.cu", "fmm_k_generic.cu", "fmm_k_stream.cu", "fmm_unfused.cu",
                 "fmm_ingest.cu"]
 HOST_SOURCES = ["fmm_plan.cpp", "fmm_mmio.cpp"]
 

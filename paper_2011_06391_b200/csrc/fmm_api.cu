@@ -10,12 +10,13 @@
 #include "fmm_kernels.cuh"
 #include "fmm_dispatch.cuh"
 #include "fmm_plan.h"
-#include "fmm_sched.cuh"
 #include "fmm_unfused.h"
 
 #include <cuda.h>
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -41,8 +42,16 @@ struct Shard {
     bool use_ext = false;  // ext may legitimately be the legacy NULL stream
     DevBuf X, Y, Z, Xb, partial;
     DevBuf H, iota;  // unfused baseline: materialised messages, edge ids
+    DevBuf hs;       // d > 1024 streamed kernel: per-edge scalar h
     cudaEvent_t ev_start = nullptr, ev_k0 = nullptr, ev_k1 = nullptr, ev_end = nullptr,
                 ev_copy = nullptr;
+    // Launches that use this shard's scratch (chunk partials, fold tickets,
+    // unfused messages) are ordered after the previous one even when the
+    // caller moved to another stream (fmm_set_stream + FMM_ASYNC): the next
+    // launch waits on ev_last when its stream differs from last_stream.
+    cudaEvent_t ev_last = nullptr;
+    cudaStream_t last_stream = nullptr;
+    bool has_last = false;
     // host-pointer FMM_ASYNC pipeline: two buffer slots, copy-in / compute /
     // copy-out on three streams, so call k's Z download overlaps call k+1's
     // X upload (PCIe is full duplex) and the kernels
@@ -58,6 +67,13 @@ struct Shard {
 
 struct fmm_ctx {
     std::vector<Shard> shards;
+    // Lifetime: graphs keep their context's shard table alive. fmm_destroy
+    // releases the device resources at once but deletes the struct only when
+    // the last graph of the context is freed, so fmm_graph_free is safe in
+    // either order (Python finalisers and C++ destructors run in arbitrary
+    // order at shutdown). Guarded by life_mu().
+    int graphs = 0;
+    bool destroyed = false;
     int variant = -1;  // kernel shape variant (FMM_VARIANT env, tuning only)
     double row_weight = 0.0;  // shard partition: 0 = part1d, > 0 = part1d_weighted
     bool p2p_ok = true;  // every pair of distinct shard devices has peer access
@@ -67,20 +83,10 @@ struct fmm_ctx {
 
 namespace {
 
-// Persistent-kernel work lists of one shard for one (gpw, u) shape.
-struct SchedDev {
-    int gpw = 0, u = 0, warps = 0;
-    int32_t* group_item_begin = nullptr;
-    int4* items = nullptr;
-    int32_t* warp_steps = nullptr;
-    int32_t* empty_rows = nullptr;
-    int64_t n_empty = 0;
-};
-
 struct GShard {
     int shard = 0;
-    std::shared_ptr<fmm::ShardPlan> plan;  // host copy, for lazily built schedules
-    std::vector<SchedDev> scheds;
+    int chunk = 256;  // edges per chunk of a split row (fast scheme)
+    int64_t edge_begin = 0;  // first edge of the shard in the uploaded CSR
     int64_t row_begin = 0, row_end = 0, nnz = 0;
     int64_t n_split_rows = 0, n_wide_rows = 0, n_chunks = 0, n_slots = 0, nonempty = 0, max_degree = 0;
     int64_t* row_ptr = nullptr;
@@ -91,6 +97,9 @@ struct GShard {
     int4* chunks = nullptr;
     int4* split_rows = nullptr;
     unsigned* split_count = nullptr;  // in-kernel fold tickets (zero between launches)
+    uint8_t* peer_mask = nullptr;     // per shard-local row: bit q = peer slot q reads it
+    int64_t exchange_rows = 0;        // sum of popcount(peer_mask) (rows sent per exchange)
+    int64_t exchange_rows_all = 0;    // rows * peers (every row to every peer)
 };
 
 }  // namespace
@@ -100,6 +109,7 @@ struct fmm_graph {
     int64_t m = 0, n = 0, nnz = 0, row_begin = 0, row_end = 0;
     int64_t max_col = -1;
     bool has_values = false;
+    bool iter_masks = false;  // fmm_iterate's halo masks were built
     std::vector<GShard> shards;
 };
 
@@ -120,6 +130,24 @@ fmm_status cuda_err(fmm_ctx* ctx, cudaError_t e, const char* what) {
         cudaError_t e_ = (call);                                     \
         if (e_ != cudaSuccess) return cuda_err((ctx), e_, #call);    \
     } while (0)
+
+std::mutex& life_mu() {
+    static std::mutex mu;
+    return mu;
+}
+
+// Scratch-using launches on a shard: wait for the previous one if it ran on
+// another stream, then (after the launch) remember this one.
+fmm_status order_scratch(fmm_ctx* ctx, Shard& sh, cudaStream_t s) {
+    if (sh.has_last && sh.last_stream != s) FMM_CK(ctx, cudaStreamWaitEvent(s, sh.ev_last, 0));
+    return FMM_OK;
+}
+fmm_status mark_scratch(fmm_ctx* ctx, Shard& sh, cudaStream_t s) {
+    FMM_CK(ctx, cudaEventRecord(sh.ev_last, s));
+    sh.last_stream = s;
+    sh.has_last = true;
+    return FMM_OK;
+}
 
 fmm_status ensure(fmm_ctx* ctx, const Shard& sh, DevBuf& b, size_t bytes) {
     if (bytes <= b.cap) return FMM_OK;
@@ -218,47 +246,87 @@ bool launch_rows(const fmm::KParams& p, int pattern, int d, bool exact, bool a32
     return fmm::launch_generic(p, d, exact, vec, s);
 }
 
-// Launch the fused kernels of one shard: rows (+ chunks) then the combine.
-// Returns the number of kernels launched, or -1 if no instantiation fits.
-// Persistent-kernel work lists for (gpw, u) on this shard, built on first use
-// from the host copy of the plan (synchronous upload, outside timed regions).
-SchedDev* get_sched(GShard& gs, int gpw, int u, int warps) {
-    for (SchedDev& sd : gs.scheds)
-        if (sd.gpw == gpw && sd.u == u && sd.warps == warps) return &sd;
-    if (!gs.plan) return nullptr;
-    const fmm::GroupSchedule S = fmm::build_group_schedule(*gs.plan, warps, gpw, u);
-    SchedDev sd;
-    sd.gpw = gpw;
-    sd.u = u;
-    sd.warps = warps;
-    sd.n_empty = static_cast<int64_t>(S.empty_rows.size());
-    std::vector<int4> items(S.items.size());
-    std::memcpy(items.data(), S.items.data(), items.size() * sizeof(int4));
-    if (upload_vec(nullptr, S.group_item_begin, &sd.group_item_begin) != FMM_OK ||
-        upload_vec(nullptr, items, &sd.items) != FMM_OK ||
-        upload_vec(nullptr, S.warp_steps, &sd.warp_steps) != FMM_OK ||
-        upload_vec(nullptr, S.empty_rows, &sd.empty_rows) != FMM_OK) {
-        for (void* q : {static_cast<void*>(sd.group_item_begin), static_cast<void*>(sd.items),
-                        static_cast<void*>(sd.warp_steps), static_cast<void*>(sd.empty_rows)})
-            if (q) cudaFree(q);
-        cudaGetLastError();
-        return nullptr;
+// need[c] = 1 for the columns shard gs's edges point at (empty vector when
+// the shard has no edges). Caller holds ctx->mu.
+fmm_status shard_column_use(fmm_ctx* ctx, const GShard& gs, int64_t n, std::vector<uint8_t>& need) {
+    need.clear();
+    if (gs.nnz == 0 || n <= 0) return FMM_OK;
+    const Shard& sh = ctx->shards[gs.shard];
+    FMM_CK(ctx, cudaSetDevice(sh.dev));
+    uint8_t* dn = nullptr;
+    FMM_CK(ctx, cudaMalloc(&dn, static_cast<size_t>(n)));
+    cudaError_t e = cudaMemset(dn, 0, static_cast<size_t>(n));
+    if (e == cudaSuccess) {
+        const int blocks = static_cast<int>(std::min<int64_t>((gs.nnz + 255) / 256, 148 * 16));
+        fmm::fmm_mark_cols_kernel<<<blocks, 256>>>(gs.col, gs.nnz, dn);
+        e = cudaGetLastError();
     }
-    gs.scheds.push_back(sd);
-    return &gs.scheds.back();
+    need.resize(static_cast<size_t>(n));
+    if (e == cudaSuccess) e = cudaMemcpy(need.data(), dn, static_cast<size_t>(n), cudaMemcpyDeviceToHost);
+    cudaFree(dn);
+    if (e != cudaSuccess) return cuda_err(ctx, e, "column use");
+    return FMM_OK;
+}
+
+// Halo masks of a multi-shard graph for fmm_iterate's fused exchange: bit
+// slot(q) of shard s's row r is set iff shard q's edges point at it, slot(q)
+// = q for q < s and q-1 above (the order of the kernel's zpeer list).
+fmm_status build_iterate_masks(fmm_ctx* ctx, fmm_graph* g) {
+    const int S = static_cast<int>(g->shards.size());
+    std::vector<std::vector<uint8_t>> need(S);
+    for (int q = 0; q < S; ++q) {
+        fmm_status st = shard_column_use(ctx, g->shards[q], g->n, need[q]);
+        if (st != FMM_OK) return st;
+    }
+    for (int s = 0; s < S; ++s) {
+        GShard& gs = g->shards[s];
+        const int64_t rows = gs.row_end - gs.row_begin;
+        std::vector<uint8_t> m(static_cast<size_t>(std::max<int64_t>(rows, 1)), 0);
+        gs.exchange_rows = 0;
+        for (int q = 0; q < S; ++q) {
+            if (q == s || need[q].empty()) continue;
+            const uint8_t bit = static_cast<uint8_t>(1u << (q < s ? q : q - 1));
+            const uint8_t* nq = need[q].data() + gs.row_begin;
+            for (int64_t r = 0; r < rows; ++r)
+                if (nq[r]) m[r] |= bit;
+        }
+        for (int64_t r = 0; r < rows; ++r) gs.exchange_rows += __builtin_popcount(m[r]);
+        gs.exchange_rows_all = rows * (S - 1);
+        FMM_CK(ctx, cudaSetDevice(ctx->shards[gs.shard].dev));
+        if (gs.peer_mask) {
+            cudaFree(gs.peer_mask);
+            gs.peer_mask = nullptr;
+        }
+        fmm_status st = upload_vec(ctx, m, &gs.peer_mask);
+        if (st != FMM_OK) return st;
+    }
+    g->iter_masks = true;
+    return FMM_OK;
+}
+
+// d > kMaxRegDim with a scalar message: the streamed kernel keeps one h per
+// edge of the shard (fmm_k_stream.cu). nullptr when not needed.
+float* hscratch(fmm_ctx* ctx, Shard& sh, const GShard& gs, int64_t d, const fmm_opspec& spec) {
+    if (d <= fmm::kMaxRegDim || spec.rop == FMM_ROP_NOOP || gs.nnz == 0) return nullptr;
+    if (ensure(ctx, sh, sh.hs, static_cast<size_t>(gs.nnz) * sizeof(float)) != FMM_OK) return nullptr;
+    return static_cast<float*>(sh.hs.ptr);
 }
 
 int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, bool exact,
                  const float* X, int64_t row0, const float* Y, float* Z, float* partial,
-                 const float* val, int variant, int num_sms, cudaStream_t stream,
-                 const fmm::PeerOut* peers = nullptr) {
+                 const float* val, int variant, cudaStream_t stream,
+                 const fmm::PeerOut* peers = nullptr, float* hs = nullptr, bool use_mask = true) {
     fmm::KParams p{};
     fmm::PeerOut po{};
     if (peers) {
         po = *peers;
         for (int q = 0; q < po.n; ++q) p.zpeer[q] = po.p[q];
         p.n_peer = po.n;
+        // halo exchange: only rows some peer reads are stored to it
+        if (use_mask && po.n > 0 && gs.peer_mask) p.peer_mask = gs.peer_mask;
+        po.mask = p.peer_mask;
     }
+    p.hbuf = hs;
     p.row_ptr = gs.row_ptr;
     p.col = gs.col;
     p.val = val;
@@ -267,7 +335,7 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
     p.Z = Z;
     p.partial = partial;
     p.row0 = row0;
-    p.chunk = gs.plan ? gs.plan->chunk : 256;
+    p.chunk = gs.chunk;
     p.d = static_cast<int>(d);
     p.vop = spec.vop; p.rop = spec.rop; p.sop = spec.sop; p.mop = spec.mop; p.aop = spec.aop;
     p.alpha = spec.alpha;
@@ -296,6 +364,18 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
         p.n_narrow_rows = rows;
     }
     if (p.n_chunk_items + p.n_wide_rows + p.n_narrow_rows == 0) return 0;
+    if (d > fmm::kMaxRegDim) {
+        // any d past the register-resident shapes: the streamed kernel tiles
+        // d (reference: the d > 256 second sweep, kernel.hpp:192-225); rows
+        // are never split, each folded by one warp in storage order
+        p.chunks = nullptr;
+        p.n_chunk_items = 0;
+        p.order = gs.order;
+        p.items = gs.items;
+        p.n_wide_rows = 0;
+        p.n_narrow_rows = rows;
+        return fmm::launch_stream(p, exact, stream) ? 1 : -1;
+    }
     const size_t a = static_cast<size_t>(d) * sizeof(float);
     const bool a16 = (d % 4 == 0) && aligned(X, 16) && aligned(Y, 16) && aligned(Z, 16) &&
                      (partial == nullptr || aligned(partial, 16)) && (a % 16 == 0);
@@ -303,51 +383,12 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
                     (partial == nullptr || aligned(partial, 8));
     bool a32 = (d % 8 == 0) && aligned(X, 32) && aligned(Y, 32) && aligned(Z, 32) &&
                (partial == nullptr || aligned(partial, 32));
-    for (int q = 0; q < po.n; ++q) a32 = a32 && aligned(po.p[q], 32);
-    // fast scheme, hot patterns: the persistent cp.async-pipelined kernel
-    int gpw = 0, su = 0;
-    const bool sched_pattern = pattern == FMM_PATTERN_SIGMOID_EMBED || pattern == FMM_PATTERN_TDIST ||
-                               pattern == FMM_PATTERN_FR_LAYOUT;
-    // FMM_VARIANT -4 / -3: persistent pipelined kernel (shape 0 / 1), opt-in:
-    // on config 2 it matches but does not beat the row kernel, both sit near
-    // the L2->SM bandwidth. -1 (default), -2, >= 0: row kernel.
-    const int sv = variant == -3 ? 1 : 0;
-    if (!exact && (variant == -4 || variant == -3) && a16 && sched_pattern && gs.nnz < INT32_MAX && po.n == 0 &&
-        fmm::sched_shape_for(static_cast<int>(d), sv, &gpw, &su)) {
-        SchedDev* sd = get_sched(gs, gpw, su, num_sms * 8);
-        if (sd) {
-            fmm::SchedParams sp{};
-            sp.col = gs.col;
-            sp.val = val;
-            sp.X = X;
-            sp.Y = Y;
-            sp.Z = Z;
-            sp.partial = partial;
-            sp.group_item_begin = sd->group_item_begin;
-            sp.items = sd->items;
-            sp.warp_steps = sd->warp_steps;
-            sp.empty_rows = sd->empty_rows;
-            sp.n_empty = sd->n_empty;
-            sp.row0 = row0;
-            sp.d = static_cast<int>(d);
-            sp.vop = spec.vop; sp.rop = spec.rop; sp.sop = spec.sop; sp.mop = spec.mop; sp.aop = spec.aop;
-            sp.alpha = spec.alpha;
-            sp.k = spec.k;
-            bool ok = false;
-            if (pattern == FMM_PATTERN_SIGMOID_EMBED) ok = fmm::launch_sched_sigmoid(sp, static_cast<int>(d), sv, num_sms, stream);
-            else if (pattern == FMM_PATTERN_TDIST) ok = fmm::launch_sched_tdist(sp, static_cast<int>(d), sv, num_sms, stream);
-            else ok = fmm::launch_sched_fr(sp, static_cast<int>(d), sv, num_sms, stream);
-            if (ok) {
-                int launches = 1;
-                if (split && gs.n_split_rows > 0) {
-                    fmm::fmm_combine_kernel<<<static_cast<unsigned>(gs.n_split_rows), 256, 0, stream>>>(
-                        gs.split_rows, partial, Z, static_cast<int>(d), spec.aop == FMM_AOP_AMAX ? 1 : 0, po);
-                    ++launches;
-                }
-                return launches;
-            }
-        }
+    bool fold4 = (d % 4 == 0) && aligned(Z, 16) && (partial == nullptr || aligned(partial, 16));
+    for (int q = 0; q < po.n; ++q) {
+        a32 = a32 && aligned(po.p[q], 32);
+        fold4 = fold4 && aligned(po.p[q], 16);
     }
+    p.fold_vec4 = fold4 ? 1 : 0;
     if (variant < -1) variant = -1;
     // split rows fold inside the row kernel (the last chunk's warp) unless
     // FMM_FOLD_KERNEL selects the separate combine kernel
@@ -368,6 +409,24 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
     return launches;
 }
 
+// Walk the dispatch tables with launch_one in attribute-query mode.
+void preload_kernels() {
+    fmm::KParams p{};
+    const int pats[] = {FMM_PATTERN_SIGMOID_EMBED, FMM_PATTERN_SPMM_GCN, FMM_PATTERN_FR_LAYOUT, FMM_PATTERN_TDIST,
+                        FMM_PATTERN_FR_ATTRACT, FMM_PATTERN_GENERIC};
+    const int dims[] = {1, 2, 4, 8, 16, 32, 64, 128, 256, 512};
+    fmm::t_preload = true;
+    for (int pat : pats)
+        for (int d : dims)
+            for (int ex = 0; ex < 2; ++ex)
+                for (int a32 = 0; a32 < 2; ++a32) launch_rows(p, pat, d, ex != 0, a32 != 0, true, true, -1, nullptr);
+    for (int ex = 0; ex < 2; ++ex) {
+        for (int d : {32, 64, 96, 128, 256, 512, 1024}) fmm::launch_generic(p, d, ex != 0, false, nullptr);
+        fmm::launch_stream(p, ex != 0, nullptr);
+    }
+    fmm::t_preload = false;
+}
+
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) return 0.f;
@@ -381,7 +440,7 @@ fmm_status check_spec(fmm_ctx* ctx, const fmm_opspec* spec, int64_t d) {
         return set_err(ctx, FMM_E_UNSUPPORTED,
                        "fused_mm: USER slot has no device kernel (no CPU fallback)");
     if (d < 1) return set_err(ctx, FMM_E_INVAL, "fused_mm: d must be >= 1");
-    if (d > 1024) return set_err(ctx, FMM_E_UNSUPPORTED, "fused_mm: d > 1024 not supported");
+    if (d > (int64_t(1) << 24)) return set_err(ctx, FMM_E_UNSUPPORTED, "fused_mm: d > 2^24 not supported");
     return FMM_OK;
 }
 
@@ -448,9 +507,12 @@ fmm_status run_host_async(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec& sp
         const float* xd = alias ? yd : static_cast<const float*>(sh.aX[k].ptr);
         const int64_t row0 = alias ? gs.row_begin : 0;
         float* zd = static_cast<float*>(sh.aZ[k].ptr);
+        float* hs = hscratch(ctx, sh, gs, d, spec);
+        if ((part || hs) && (st = order_scratch(ctx, sh, cs)) != FMM_OK) return st;
         const int l = launch_shard(const_cast<GShard&>(gs), spec, pattern, d, exact, xd, row0, yd, zd, part,
-                                   gs.val, ctx->variant, sh.num_sms, cs);
+                                   gs.val, ctx->variant, cs, nullptr, hs);
         if (l < 0) return set_err(ctx, FMM_E_UNSUPPORTED, "fused_mm: no kernel for this d / alignment");
+        if ((part || hs) && (st = mark_scratch(ctx, sh, cs)) != FMM_OK) return st;
         launches += l;
         FMM_CK(ctx, cudaGetLastError());
         FMM_CK(ctx, cudaEventRecord(sh.ev_comp[k], cs));
@@ -495,6 +557,7 @@ fmm_status fmm_host_free(void* ptr) {
 fmm_status fmm_sync(fmm_ctx* ctx) {
     if (!ctx) return FMM_E_INVAL;
     std::lock_guard<std::mutex> lk(ctx->mu);
+    if (ctx->destroyed) return set_err(ctx, FMM_E_INVAL, "context was destroyed");
     for (Shard& sh : ctx->shards) {
         FMM_CK(ctx, cudaSetDevice(sh.dev));
         if (sh.s_in) FMM_CK(ctx, cudaStreamSynchronize(sh.s_in));
@@ -548,10 +611,25 @@ fmm_status fmm_create(int ngpu, const int* devs, fmm_ctx** out) {
             cudaStreamCreateWithFlags(&sh.own, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreate(&sh.ev_start) != cudaSuccess || cudaEventCreate(&sh.ev_k0) != cudaSuccess ||
             cudaEventCreate(&sh.ev_k1) != cudaSuccess || cudaEventCreate(&sh.ev_end) != cudaSuccess ||
-            cudaEventCreateWithFlags(&sh.ev_copy, cudaEventDisableTiming) != cudaSuccess) {
+            cudaEventCreateWithFlags(&sh.ev_copy, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&sh.ev_last, cudaEventDisableTiming) != cudaSuccess) {
             fmm_destroy(ctx);
             return FMM_E_CUDA;
         }
+    }
+    // load every shipped row kernel now (CUDA loads modules lazily, ~10 ms
+    // per op kind on the first launch otherwise: the drop-in's first
+    // fused_mm call would pay it); FMM_NO_PRELOAD=1 skips
+    if (!std::getenv("FMM_NO_PRELOAD")) {
+        std::vector<int> seen;
+        for (int i = 0; i < ngpu; ++i) {
+            const int dev = ctx->shards[i].dev;
+            if (std::find(seen.begin(), seen.end(), dev) != seen.end()) continue;
+            seen.push_back(dev);
+            cudaSetDevice(dev);
+            preload_kernels();
+        }
+        cudaGetLastError();
     }
     // peer access between distinct devices (NVLink / NVSwitch)
     for (int i = 0; i < ngpu; ++i)
@@ -575,21 +653,43 @@ fmm_status fmm_create(int ngpu, const int* devs, fmm_ctx** out) {
 
 fmm_status fmm_destroy(fmm_ctx* ctx) {
     if (!ctx) return FMM_E_INVAL;
-    for (Shard& sh : ctx->shards) {
-        cudaSetDevice(sh.dev);
-        if (sh.own) cudaStreamSynchronize(sh.own);
-        for (cudaStream_t st : {sh.s_in, sh.s_out})
-            if (st) cudaStreamSynchronize(st);
-        for (DevBuf* b : {&sh.X, &sh.Y, &sh.Z, &sh.Xb, &sh.partial, &sh.H, &sh.iota, &sh.aX[0], &sh.aX[1], &sh.aY[0],
-                          &sh.aY[1], &sh.aZ[0], &sh.aZ[1]})
-            if (b->ptr) cudaFree(b->ptr);
-        for (cudaEvent_t e : {sh.ev_start, sh.ev_k0, sh.ev_k1, sh.ev_end, sh.ev_copy, sh.ev_in[0], sh.ev_in[1],
-                              sh.ev_comp[0], sh.ev_comp[1], sh.ev_out[0], sh.ev_out[1]})
-            if (e) cudaEventDestroy(e);
-        for (cudaStream_t st : {sh.own, sh.s_in, sh.s_out})
-            if (st) cudaStreamDestroy(st);
+    std::lock_guard<std::mutex> life(life_mu());
+    if (ctx->destroyed) return FMM_E_INVAL;
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        for (Shard& sh : ctx->shards) {
+            cudaSetDevice(sh.dev);
+            if (sh.own) cudaStreamSynchronize(sh.own);
+            if (sh.use_ext) cudaStreamSynchronize(sh.ext);
+            for (cudaStream_t st : {sh.s_in, sh.s_out})
+                if (st) cudaStreamSynchronize(st);
+            for (DevBuf* b : {&sh.X, &sh.Y, &sh.Z, &sh.Xb, &sh.partial, &sh.H, &sh.iota, &sh.hs, &sh.aX[0],
+                              &sh.aX[1], &sh.aY[0], &sh.aY[1], &sh.aZ[0], &sh.aZ[1]})
+                if (b->ptr) {
+                    cudaFree(b->ptr);
+                    b->ptr = nullptr;
+                    b->cap = 0;
+                }
+            for (cudaEvent_t* e : {&sh.ev_start, &sh.ev_k0, &sh.ev_k1, &sh.ev_end, &sh.ev_copy, &sh.ev_last,
+                                   &sh.ev_in[0], &sh.ev_in[1], &sh.ev_comp[0], &sh.ev_comp[1], &sh.ev_out[0],
+                                   &sh.ev_out[1]})
+                if (*e) {
+                    cudaEventDestroy(*e);
+                    *e = nullptr;
+                }
+            for (cudaStream_t* st : {&sh.own, &sh.s_in, &sh.s_out})
+                if (*st) {
+                    cudaStreamDestroy(*st);
+                    *st = nullptr;
+                }
+            sh.use_ext = false;
+            sh.has_last = false;
+        }
+        ctx->destroyed = true;
     }
-    delete ctx;
+    // graphs still alive keep the (now resource-free) shard table until the
+    // last of them is freed
+    if (ctx->graphs == 0) delete ctx;
     return FMM_OK;
 }
 
@@ -598,6 +698,7 @@ const char* fmm_last_error(const fmm_ctx* ctx) { return ctx ? ctx->err.c_str() :
 fmm_status fmm_set_stream(fmm_ctx* ctx, int shard, void* stream) {
     if (!ctx || shard < 0 || shard >= static_cast<int>(ctx->shards.size())) return FMM_E_INVAL;
     std::lock_guard<std::mutex> lk(ctx->mu);
+    if (ctx->destroyed) return set_err(ctx, FMM_E_INVAL, "context was destroyed");
     ctx->shards[shard].ext = static_cast<cudaStream_t>(stream);
     ctx->shards[shard].use_ext = true;
     return FMM_OK;
@@ -606,6 +707,7 @@ fmm_status fmm_set_stream(fmm_ctx* ctx, int shard, void* stream) {
 fmm_status fmm_set_variant(fmm_ctx* ctx, int variant) {
     if (!ctx || variant < -6 || variant > 63) return FMM_E_INVAL;
     std::lock_guard<std::mutex> lk(ctx->mu);
+    if (ctx->destroyed) return set_err(ctx, FMM_E_INVAL, "context was destroyed");
     ctx->variant = variant;
     return FMM_OK;
 }
@@ -615,6 +717,7 @@ int fmm_get_variant(const fmm_ctx* ctx) { return ctx ? ctx->variant : -1; }
 fmm_status fmm_reset_stream(fmm_ctx* ctx, int shard) {
     if (!ctx || shard < 0 || shard >= static_cast<int>(ctx->shards.size())) return FMM_E_INVAL;
     std::lock_guard<std::mutex> lk(ctx->mu);
+    if (ctx->destroyed) return set_err(ctx, FMM_E_INVAL, "context was destroyed");
     ctx->shards[shard].ext = nullptr;
     ctx->shards[shard].use_ext = false;
     return FMM_OK;
@@ -641,6 +744,7 @@ fmm_status fmm_part1d_weighted(int64_t m, const int64_t* row_ptr, int t, double 
 fmm_status fmm_set_row_weight(fmm_ctx* ctx, double row_weight) {
     if (!ctx || !(row_weight >= 0.0)) return FMM_E_INVAL;
     std::lock_guard<std::mutex> lk(ctx->mu);
+    if (ctx->destroyed) return set_err(ctx, FMM_E_INVAL, "context was destroyed");
     ctx->row_weight = row_weight;
     return FMM_OK;
 }
@@ -661,6 +765,7 @@ fmm_status fmm_graph_upload(fmm_ctx* ctx, int64_t m, int64_t n, const int64_t* r
                             int64_t row_end, fmm_graph** out) {
     if (!ctx || !out) return FMM_E_INVAL;
     std::lock_guard<std::mutex> lk(ctx->mu);
+    if (ctx->destroyed) return set_err(ctx, FMM_E_INVAL, "context was destroyed");
     *out = nullptr;
     if (m < 0 || n < 0 || !row_ptr) return set_err(ctx, FMM_E_INVAL, "graph_upload: bad sizes");
     if (n > INT32_MAX) return set_err(ctx, FMM_E_UNSUPPORTED, "graph_upload: n >= 2^31");
@@ -673,6 +778,10 @@ fmm_status fmm_graph_upload(fmm_ctx* ctx, int64_t m, int64_t n, const int64_t* r
     fmm_graph* g = new (std::nothrow) fmm_graph();
     if (!g) return FMM_E_OOM;
     g->ctx = ctx;
+    {
+        std::lock_guard<std::mutex> life(life_mu());
+        ++ctx->graphs;  // fmm_graph_free (also on the error paths below) releases it
+    }
     g->m = m;
     g->n = n;
     g->row_begin = row_begin;
@@ -708,7 +817,8 @@ fmm_status fmm_graph_upload(fmm_ctx* ctx, int64_t m, int64_t n, const int64_t* r
             break;
         }
         gs.nnz = P.nnz;
-        gs.plan = std::make_shared<fmm::ShardPlan>(P);
+        gs.chunk = P.chunk;
+        gs.edge_begin = P.edge_begin;
         gs.n_split_rows = P.n_split_rows;
         gs.n_wide_rows = P.n_wide_rows;
         gs.n_chunks = static_cast<int64_t>(P.chunks.size());
@@ -774,22 +884,130 @@ fmm_status fmm_graph_upload(fmm_ctx* ctx, int64_t m, int64_t n, const int64_t* r
     return FMM_OK;
 }
 
+fmm_status fmm_graph_column_use(const fmm_graph* g, uint8_t* need) {
+    if (!g || !need) return FMM_E_INVAL;
+    fmm_ctx* ctx = g->ctx;
+    if (ctx->destroyed) return FMM_E_INVAL;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    std::memset(need, 0, static_cast<size_t>(std::max<int64_t>(g->n, 0)));
+    std::vector<uint8_t> part;
+    for (const GShard& gs : g->shards) {
+        fmm_status st = shard_column_use(ctx, gs, g->n, part);
+        if (st != FMM_OK) return st;
+        if (!part.empty())
+            for (int64_t c = 0; c < g->n; ++c) need[c] |= part[c];
+    }
+    return FMM_OK;
+}
+
+fmm_status fmm_graph_set_peer_mask(fmm_graph* g, const uint8_t* mask, int npeer) {
+    if (!g || npeer < 0 || npeer > fmm::kMaxPeers) return FMM_E_INVAL;
+    fmm_ctx* ctx = g->ctx;
+    if (ctx->destroyed) return FMM_E_INVAL;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (g->shards.size() != 1) return set_err(ctx, FMM_E_INVAL, "set_peer_mask: single-shard graphs only");
+    GShard& gs = g->shards[0];
+    FMM_CK(ctx, cudaSetDevice(ctx->shards[gs.shard].dev));
+    if (gs.peer_mask) {
+        FMM_CK(ctx, cudaDeviceSynchronize());  // a launch may still read it
+        cudaFree(gs.peer_mask);
+        gs.peer_mask = nullptr;
+    }
+    gs.exchange_rows = gs.exchange_rows_all = 0;
+    if (!mask) return FMM_OK;  // cleared: every row to every peer
+    const int64_t rows = gs.row_end - gs.row_begin;
+    const unsigned keep = npeer >= 8 ? 0xffu : ((1u << npeer) - 1u);
+    std::vector<uint8_t> m(static_cast<size_t>(std::max<int64_t>(rows, 1)), 0);
+    for (int64_t r = 0; r < rows; ++r) {
+        m[r] = static_cast<uint8_t>(mask[r] & keep);
+        gs.exchange_rows += __builtin_popcount(m[r]);
+    }
+    gs.exchange_rows_all = rows * npeer;
+    fmm_status st = upload_vec(ctx, m, &gs.peer_mask);
+    return st;
+}
+
 fmm_status fmm_graph_free(fmm_graph* g) {
     if (!g) return FMM_E_INVAL;
+    fmm_ctx* ctx = g->ctx;
     for (GShard& gs : g->shards) {
-        cudaSetDevice(g->ctx->shards[gs.shard].dev);
-        for (SchedDev& sd : gs.scheds)
-            for (void* q : {static_cast<void*>(sd.group_item_begin), static_cast<void*>(sd.items),
-                            static_cast<void*>(sd.warp_steps), static_cast<void*>(sd.empty_rows)})
-                if (q) cudaFree(q);
+        cudaSetDevice(ctx->shards[gs.shard].dev);
         for (void* p : {static_cast<void*>(gs.row_ptr), static_cast<void*>(gs.col), static_cast<void*>(gs.val),
                         static_cast<void*>(gs.order), static_cast<void*>(gs.items), static_cast<void*>(gs.chunks),
-                        static_cast<void*>(gs.split_count),
-                        static_cast<void*>(gs.split_rows)})
+                        static_cast<void*>(gs.split_count), static_cast<void*>(gs.split_rows),
+                        static_cast<void*>(gs.peer_mask)})
             if (p) cudaFree(p);
     }
     delete g;
+    std::lock_guard<std::mutex> life(life_mu());
+    if (--ctx->graphs == 0 && ctx->destroyed) delete ctx;
     return FMM_OK;
+}
+
+fmm_status fmm_graph_update_values(fmm_graph* g, const float* values) {
+    if (!g) return FMM_E_INVAL;
+    fmm_ctx* ctx = g->ctx;
+    if (ctx->destroyed) return FMM_E_INVAL;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    for (GShard& gs : g->shards) {
+        Shard& sh = ctx->shards[gs.shard];
+        FMM_CK(ctx, cudaSetDevice(sh.dev));
+        // a launch still in flight may read the old values
+        FMM_CK(ctx, cudaStreamSynchronize(sh.stream()));
+        if (!values) {
+            if (gs.val) cudaFree(gs.val);
+            gs.val = nullptr;
+            continue;
+        }
+        if (gs.nnz == 0) continue;
+        if (!gs.val) FMM_CK(ctx, cudaMalloc(&gs.val, gs.nnz * sizeof(float)));
+        FMM_CK(ctx, cudaMemcpy(gs.val, values + gs.edge_begin, gs.nnz * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    g->has_values = values != nullptr;
+    return FMM_OK;
+}
+
+uint64_t fmm_fingerprint(const void* data, size_t bytes) {
+    if (!data || bytes == 0) return 0x9e3779b97f4a7c15ull ^ bytes;
+    const unsigned char* b = static_cast<const unsigned char*>(data);
+    constexpr size_t kChunk = size_t(1) << 22;  // 4 MiB per task, combined in order
+    const size_t nchunk = (bytes + kChunk - 1) / kChunk;
+    std::vector<uint64_t> h(nchunk);
+    auto hash_chunk = [&](size_t c) {
+        const size_t lo = c * kChunk, hi = std::min(bytes, lo + kChunk);
+        uint64_t a = 0x243f6a8885a308d3ull ^ lo, z = 0x13198a2e03707344ull;
+        size_t i = lo;
+        for (; i + 16 <= hi; i += 16) {
+            uint64_t w0, w1;
+            std::memcpy(&w0, b + i, 8);
+            std::memcpy(&w1, b + i + 8, 8);
+            a = (a ^ w0) * 0x9fb21c651e98df25ull;
+            z = (z ^ w1) * 0xc2b2ae3d27d4eb4full;
+            a ^= a >> 29;
+            z ^= z >> 31;
+        }
+        for (; i < hi; ++i) a = (a ^ b[i]) * 0x100000001b3ull;
+        h[c] = a * 0xff51afd7ed558ccdull ^ z;
+    };
+    const unsigned nt = std::max(1u, std::min<unsigned>(static_cast<unsigned>(nchunk),
+                                                        std::thread::hardware_concurrency()));
+    if (nt == 1) {
+        for (size_t c = 0; c < nchunk; ++c) hash_chunk(c);
+    } else {
+        std::atomic<size_t> next{0};
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < nt; ++t)
+            th.emplace_back([&] {
+                for (size_t c; (c = next.fetch_add(1)) < nchunk;) hash_chunk(c);
+            });
+        for (auto& x : th) x.join();
+    }
+    uint64_t out = 0xcbf29ce484222325ull ^ bytes;
+    for (uint64_t v : h) {
+        out = (out ^ v) * 0x9e3779b97f4a7c15ull;
+        out ^= out >> 32;
+    }
+    return out;
 }
 
 fmm_status fmm_graph_get_info(const fmm_graph* g, fmm_graph_info* out) {
@@ -803,6 +1021,8 @@ fmm_status fmm_graph_get_info(const fmm_graph* g, fmm_graph_info* out) {
     I.shards = static_cast<int32_t>(g->shards.size());
     I.has_values = g->has_values ? 1 : 0;
     for (const GShard& gs : g->shards) {
+        I.exchange_rows += gs.exchange_rows;
+        I.exchange_rows_all += gs.exchange_rows_all;
         I.nonempty_rows += gs.nonempty;
         I.max_degree = std::max(I.max_degree, gs.max_degree);
         I.split_rows += gs.n_split_rows;
@@ -830,6 +1050,7 @@ fmm_status run_impl(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec, in
                     const fmm::PeerOut* peers) {
     if (!ctx || !g || g->ctx != ctx) return FMM_E_INVAL;
     std::lock_guard<std::mutex> lk(ctx->mu);
+    if (ctx->destroyed) return set_err(ctx, FMM_E_INVAL, "context was destroyed");
     fmm_status st = check_spec(ctx, spec, d);
     if (st != FMM_OK) return st;
     const int64_t rows = g->row_end - g->row_begin;
@@ -897,9 +1118,13 @@ fmm_status run_impl(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec, in
             aux = std::max(aux, pb);
         }
         if (timed) FMM_CK(ctx, cudaEventRecord(sh.ev_k0, stream));
+        float* hs = hscratch(ctx, sh, gs, d, *spec);
+        if ((part || hs) && (st = order_scratch(ctx, sh, stream)) != FMM_OK) return st;
         const int l = launch_shard(const_cast<GShard&>(gs), *spec, pattern, d, exact, xd, row0, yd, zd, part,
-                                   gs.val, ctx->variant, sh.num_sms, stream, dev_ptrs ? peers : nullptr);
+                                   gs.val, ctx->variant, stream, dev_ptrs ? peers : nullptr, hs,
+                                   (flags & FMM_PEERS_ALL) == 0);
         if (l < 0) return set_err(ctx, FMM_E_UNSUPPORTED, "fused_mm: no kernel for this d / alignment");
+        if ((part || hs) && (st = mark_scratch(ctx, sh, stream)) != FMM_OK) return st;
         launches += l;
         FMM_CK(ctx, cudaGetLastError());
         if (timed) FMM_CK(ctx, cudaEventRecord(sh.ev_k1, stream));
@@ -1015,6 +1240,7 @@ fmm_status fmm_run_unfused(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* s
                            fmm_stats* stats) {
     if (!ctx || !g || g->ctx != ctx) return FMM_E_INVAL;
     std::lock_guard<std::mutex> lk(ctx->mu);
+    if (ctx->destroyed) return set_err(ctx, FMM_E_INVAL, "context was destroyed");
     fmm_status st = check_spec(ctx, spec, d);
     if (st != FMM_OK) return st;
     if (!(flags & FMM_DEVICE_PTRS) || ctx->shards.size() != 1)
@@ -1034,6 +1260,7 @@ fmm_status fmm_run_unfused(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* s
     if ((st = ensure(ctx, sh, sh.H, hbytes)) != FMM_OK) return st;
     size_t aux = hbytes;
     const bool timed = stats != nullptr && !(flags & FMM_ASYNC);
+    if ((st = order_scratch(ctx, sh, stream)) != FMM_OK) return st;
     if (timed) FMM_CK(ctx, cudaEventRecord(sh.ev_k0, stream));
     // phase 1: SDDMM, H materialised in HBM
     fmm::SddmmParams sp{};
@@ -1080,9 +1307,9 @@ fmm_status fmm_run_unfused(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* s
         part = static_cast<float*>(sh.partial.ptr);
     }
     const int l = launch_shard(g2, sp2, pattern_of(sp2), d, /*exact=*/false, X, gs.row_begin, Ysrc, Z, part,
-                               vals, ctx->variant, sh.num_sms, stream);
-    g2.scheds.clear();
+                               vals, ctx->variant, stream);
     if (l < 0) return set_err(ctx, FMM_E_UNSUPPORTED, "unfused: no SpMM kernel");
+    if ((st = mark_scratch(ctx, sh, stream)) != FMM_OK) return st;
     launches += l;
     FMM_CK(ctx, cudaGetLastError());
     float kms = 0.f;
@@ -1110,6 +1337,7 @@ fmm_status fmm_iterate(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec,
                        float* X, int iters, uint32_t flags, fmm_stats* stats) {
     if (!ctx || !g || g->ctx != ctx) return FMM_E_INVAL;
     std::lock_guard<std::mutex> lk(ctx->mu);
+    if (ctx->destroyed) return set_err(ctx, FMM_E_INVAL, "context was destroyed");
     fmm_status st = check_spec(ctx, spec, d);
     if (st != FMM_OK) return st;
     if (iters < 0) return set_err(ctx, FMM_E_INVAL, "iterate: iters must be >= 0");
@@ -1152,6 +1380,10 @@ fmm_status fmm_iterate(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec,
     // the compute; kernel completion (events) orders the next iteration.
     // FMM_EXCHANGE_COPIES: post-kernel cudaMemcpyPeerAsync slices instead.
     const bool fused = S > 1 && S - 1 <= fmm::kMaxPeers && ctx->p2p_ok && !(flags & FMM_EXCHANGE_COPIES);
+    // halo exchange: rows no other shard reads are never sent (R-MAT
+    // configs: every empty row, plus rows referenced only locally)
+    if (fused && iters > 1 && !g->iter_masks && (st = build_iterate_masks(ctx, const_cast<fmm_graph*>(g))) != FMM_OK)
+        return st;
     int cur = 0;  // 0: Y holds the iterate, 1: Xb holds it
     for (int it = 0; it < iters; ++it) {
         const bool exchange = it + 1 < iters && S > 1;
@@ -1171,14 +1403,28 @@ fmm_status fmm_iterate(fmm_ctx* ctx, const fmm_graph* g, const fmm_opspec* spec,
                     Shard& sq = ctx->shards[g->shards[q].shard];
                     po.p[po.n++] = static_cast<float*>(cur == 0 ? sq.Xb.ptr : sq.Y.ptr) + gs.row_begin * d;
                 }
+            float* part = static_cast<float*>(sh.partial.ptr);
+            float* hs = hscratch(ctx, sh, gs, d, *spec);
+            if ((part || hs) && (st = order_scratch(ctx, sh, sh.stream())) != FMM_OK) return st;
             const int l = launch_shard(const_cast<GShard&>(gs), *spec, pattern, d, exact, xc, gs.row_begin, xc,
-                                       xn + gs.row_begin * d, static_cast<float*>(sh.partial.ptr),
-                                       gs.val, ctx->variant, sh.num_sms, sh.stream(), &po);
+                                       xn + gs.row_begin * d, part, gs.val, ctx->variant, sh.stream(),
+                                       &po, hs, !(flags & FMM_PEERS_ALL));
             if (l < 0) return set_err(ctx, FMM_E_UNSUPPORTED, "iterate: no kernel for this d / alignment");
+            if ((part || hs) && (st = mark_scratch(ctx, sh, sh.stream())) != FMM_OK) return st;
             launches += l;
             FMM_CK(ctx, cudaGetLastError());
-            if (fused && exchange) FMM_CK(ctx, cudaEventRecord(sh.ev_copy, sh.stream()));
         }
+        // ev_copy of every shard is recorded only after all shards' kernels
+        // of this iteration were enqueued: a record inside the launch loop
+        // would make shard s's kernel wait for shard q < s's kernel of the
+        // SAME iteration (the wait takes the most recent record) and
+        // serialise the shards
+        if (fused && exchange)
+            for (int s = 0; s < S; ++s) {
+                Shard& sh = ctx->shards[g->shards[s].shard];
+                FMM_CK(ctx, cudaSetDevice(sh.dev));
+                FMM_CK(ctx, cudaEventRecord(sh.ev_copy, sh.stream()));
+            }
         if (exchange && !fused) {
             // exchange: every shard pushes its fresh Z slice into every peer's next buffer
             for (int s = 0; s < S; ++s) {

@@ -7,8 +7,18 @@
 
 namespace fmm {
 
+// Set while fmm_create walks the dispatch tables: launch_one then only
+// queries the kernel's attributes, which makes CUDA's lazy module loading
+// load it now rather than inside the caller's first fused_mm call.
+inline thread_local bool t_preload = false;
+
 template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED, int MINB = 0, int PF = -1>
 inline void launch_one(const KParams& p, const Ops& ops, cudaStream_t stream) {
+    if (t_preload) {
+        cudaFuncAttributes a;
+        cudaFuncGetAttributes(&a, fmm_rows_kernel<Ops, LPG, VEC, NV, UNROLL, EXACT, MASKED, MINB, PF>);
+        return;
+    }
     constexpr int kThreads = 256;
     constexpr int GPW = 32 / LPG;
     const int64_t wide = EXACT ? 0 : p.n_chunk_items + p.n_wide_rows;
@@ -20,44 +30,48 @@ inline void launch_one(const KParams& p, const Ops& ops, cudaStream_t stream) {
 }
 
 // Vectorised shapes: d = LPG * VEC * NV exactly, rows VEC*4-byte aligned.
-// variant < 0 selects the default shape for d; others exist for tuning.
+// variant < 0 selects the default shape for d. The shipped library holds the
+// defaults plus one alternative (variant 20: the VEC = 4 shapes even when
+// rows are 32-byte aligned); the tuning alternatives swept in r01-r08
+// (tests/sweep_variants.py) compile only with -DFMM_TUNING_VARIANTS
+// (FMM_TUNING=1 python -m paper_2011_06391_b200.build), so the .so stays small
+// and its modules load fast. Unknown variants fall back to the default.
 // 256-bit shapes (VEC = 8; rows 32-byte aligned, d % 8 == 0): twice the bytes
-// per gather request of the VEC = 4 shapes. variant 20 selects the VEC = 4
-// default instead, 21-23 are tuning alternatives.
+// per gather request of the VEC = 4 shapes.
 template <class Ops, bool EXACT>
 inline bool launch_aligned32(const KParams& p, const Ops& ops, int d, int variant, cudaStream_t s) {
+    (void)variant;
     switch (d) {
         case 32:
+#ifdef FMM_TUNING_VARIANTS
             if constexpr (!EXACT) {
                 if (variant == 21) { launch_one<Ops, 2, 8, 2, 4, EXACT, false, 3, 1>(p, ops, s); return true; }
                 if (variant == 22) { launch_one<Ops, 4, 8, 1, 8, EXACT, false, 3, 1>(p, ops, s); return true; }
                 if (variant == 23) { launch_one<Ops, 4, 8, 1, 4, EXACT, false, 4, 1>(p, ops, s); return true; }
-                if (variant == 24) { launch_one<Ops, 4, 8, 1, 4, EXACT, false, 3, 1>(p, ops, s); return true; }
-                if (variant == 25) { launch_one<Ops, 4, 8, 1, 2, EXACT, false, 4, 1>(p, ops, s); return true; }
             }
+#endif
             // config 3 keeps the VEC = 4 shape (0.616 ms; VEC = 8 U = 2: 0.618)
             return false;
         case 64:
             launch_one<Ops, 8, 8, 1, 4, EXACT, false>(p, ops, s); return true;  // config 1
         case 128:
             if constexpr (!EXACT) {
+#ifdef FMM_TUNING_VARIANTS
                 if (variant == 21) { launch_one<Ops, 4, 8, 4, 4, EXACT, false>(p, ops, s); return true; }
                 if (variant == 22) { launch_one<Ops, 16, 8, 1, 4, EXACT, false>(p, ops, s); return true; }
                 if (variant == 23) { launch_one<Ops, 8, 8, 2, 2, EXACT, false>(p, ops, s); return true; }
                 if (variant == 24) { launch_one<Ops, 8, 8, 2, 4, EXACT, false, 3>(p, ops, s); return true; }
-                if (variant == 25) { launch_one<Ops, 8, 8, 2, 2, EXACT, false, 3>(p, ops, s); return true; }
-                if (variant == 26) { launch_one<Ops, 16, 8, 1, 4, EXACT, false, 3>(p, ops, s); return true; }
-                if (variant == 27) { launch_one<Ops, 16, 8, 1, 2, EXACT, false, 4>(p, ops, s); return true; }
+#endif
                 launch_one<Ops, 8, 8, 2, 4, EXACT, false>(p, ops, s); return true;  // config 2
             }
             launch_one<Ops, 8, 8, 2, 2, EXACT, false>(p, ops, s); return true;
         case 256:
             if constexpr (!EXACT) {
+#ifdef FMM_TUNING_VARIANTS
                 if (variant == 21) { launch_one<Ops, 16, 8, 2, 4, EXACT, false>(p, ops, s); return true; }
                 if (variant == 22) { launch_one<Ops, 8, 8, 4, 2, EXACT, false>(p, ops, s); return true; }
-                if (variant == 23) { launch_one<Ops, 16, 8, 2, 2, EXACT, false>(p, ops, s); return true; }
-                if (variant == 24) { launch_one<Ops, 16, 8, 2, 4, EXACT, false, 2>(p, ops, s); return true; }
                 if (variant == 25) { launch_one<Ops, 32, 8, 1, 8, EXACT, false>(p, ops, s); return true; }
+#endif
                 // config 5: a warp per row-group of 32 lanes x 32 B (80 registers)
                 launch_one<Ops, 32, 8, 1, 4, EXACT, false>(p, ops, s); return true;
             }
@@ -68,16 +82,15 @@ inline bool launch_aligned32(const KParams& p, const Ops& ops, int d, int varian
 
 template <class Ops, bool EXACT>
 inline bool launch_aligned(const KParams& p, const Ops& ops, int d, int variant, cudaStream_t s) {
+    (void)variant;
     switch (d) {
         case 1: launch_one<Ops, 1, 1, 1, 8, EXACT, false>(p, ops, s); return true;
         case 2:
-            if (variant == 1) { launch_one<Ops, 1, 2, 1, 4, EXACT, false>(p, ops, s); return true; }
-            if (variant == 2) { launch_one<Ops, 1, 2, 1, 16, EXACT, false>(p, ops, s); return true; }
-            if (variant == 6) { launch_one<Ops, 1, 2, 1, 8, EXACT, false, 6>(p, ops, s); return true; }
+#ifdef FMM_TUNING_VARIANTS
             if (variant == 0) { launch_one<Ops, 1, 2, 1, 8, EXACT, false>(p, ops, s); return true; }
             if (variant == 3) { launch_one<Ops, 1, 2, 1, 2, EXACT, false, 8>(p, ops, s); return true; }
-            if (variant == 4) { launch_one<Ops, 1, 2, 1, 8, EXACT, false, 8>(p, ops, s); return true; }
             if (variant == 5) { launch_one<Ops, 1, 2, 1, 4, EXACT, false, 8>(p, ops, s); return true; }
+#endif
             // config 4: with the index slots read through L1 the register cap
             // of 8 blocks/SM no longer pays (0.0963 vs 0.0983 ms, r08f)
             launch_one<Ops, 1, 2, 1, 4, EXACT, false>(p, ops, s); return true;
@@ -86,50 +99,37 @@ inline bool launch_aligned(const KParams& p, const Ops& ops, int d, int variant,
         case 16: launch_one<Ops, 4, 4, 1, 8, EXACT, false>(p, ops, s); return true;
         case 32:
             if constexpr (!EXACT) {
+#ifdef FMM_TUNING_VARIANTS
                 if (variant == 0) { launch_one<Ops, 8, 4, 1, 8, EXACT, false>(p, ops, s); return true; }
-                if (variant == 2) { launch_one<Ops, 2, 4, 4, 4, EXACT, false>(p, ops, s); return true; }
-                if (variant == 3) { launch_one<Ops, 8, 4, 1, 16, EXACT, false>(p, ops, s); return true; }
-                if (variant == 4) { launch_one<Ops, 4, 4, 2, 8, EXACT, false>(p, ops, s); return true; }
-                if (variant == 5) { launch_one<Ops, 2, 4, 4, 2, EXACT, false>(p, ops, s); return true; }
                 if (variant == 1) { launch_one<Ops, 4, 4, 2, 4, EXACT, false>(p, ops, s); return true; }
-                if (variant == 7) { launch_one<Ops, 4, 4, 2, 8, EXACT, false, 3>(p, ops, s); return true; }
+                if (variant == 4) { launch_one<Ops, 4, 4, 2, 8, EXACT, false>(p, ops, s); return true; }
                 if (variant == 8) { launch_one<Ops, 4, 4, 2, 4, EXACT, false, 4, 1>(p, ops, s); return true; }
-                if (variant == 9) { launch_one<Ops, 4, 4, 2, 4, EXACT, false, 4>(p, ops, s); return true; }
-                if (variant == 10) { launch_one<Ops, 4, 4, 2, 4, EXACT, false, 0, 1>(p, ops, s); return true; }
-                if (variant == 11) { launch_one<Ops, 8, 4, 1, 8, EXACT, false, 4, 1>(p, ops, s); return true; }
-                if (variant == 12) { launch_one<Ops, 4, 4, 2, 4, EXACT, false, 3, 1>(p, ops, s); return true; }
+#endif
                 // config 3: U = 2 at 4 blocks/SM (32 warps) with the column
                 // prefetch (0.616 ms; U = 4 at 3 blocks/SM: 0.646 ms)
                 launch_one<Ops, 4, 4, 2, 2, EXACT, false, 4, 1>(p, ops, s); return true;
             }
             launch_one<Ops, 4, 4, 2, 4, EXACT, false>(p, ops, s); return true;
         case 64:
-            if constexpr (!EXACT) {
-                if (variant == 0) { launch_one<Ops, 16, 4, 1, 8, EXACT, false>(p, ops, s); return true; }
-                if (variant == 2) { launch_one<Ops, 4, 4, 4, 4, EXACT, false>(p, ops, s); return true; }
-            }
             launch_one<Ops, 8, 4, 2, 4, EXACT, false>(p, ops, s); return true;
         case 128:
             if constexpr (!EXACT) {
+#ifdef FMM_TUNING_VARIANTS
                 if (variant == 0) { launch_one<Ops, 32, 4, 1, 8, EXACT, false>(p, ops, s); return true; }
                 if (variant == 1) { launch_one<Ops, 8, 4, 4, 2, EXACT, false>(p, ops, s); return true; }
                 if (variant == 3) { launch_one<Ops, 16, 4, 2, 4, EXACT, false>(p, ops, s); return true; }
-                if (variant == 4) { launch_one<Ops, 4, 4, 8, 2, EXACT, false>(p, ops, s); return true; }
-                if (variant == 5) { launch_one<Ops, 8, 4, 4, 8, EXACT, false>(p, ops, s); return true; }
-                if (variant == 6) { launch_one<Ops, 8, 4, 4, 4, EXACT, false, 3>(p, ops, s); return true; }
-                if (variant == 7) { launch_one<Ops, 8, 4, 4, 2, EXACT, false, 4>(p, ops, s); return true; }
+#endif
                 launch_one<Ops, 8, 4, 4, 4, EXACT, false>(p, ops, s); return true;
             }
             launch_one<Ops, 8, 4, 4, 2, EXACT, false>(p, ops, s); return true;
         case 256:
             if constexpr (!EXACT) {
+#ifdef FMM_TUNING_VARIANTS
                 if (variant == 0) { launch_one<Ops, 32, 4, 2, 4, EXACT, false>(p, ops, s); return true; }
-                if (variant == 2) { launch_one<Ops, 8, 4, 8, 1, EXACT, false>(p, ops, s); return true; }
-                if (variant == 6) { launch_one<Ops, 16, 4, 4, 2, EXACT, false, 2>(p, ops, s); return true; }
-                if (variant == 7) { launch_one<Ops, 16, 4, 4, 2, EXACT, false>(p, ops, s); return true; }
                 if (variant == 1) { launch_one<Ops, 8, 4, 8, 2, EXACT, false>(p, ops, s); return true; }
-                if (variant == 5) { launch_one<Ops, 32, 4, 2, 8, EXACT, false>(p, ops, s); return true; }
-                launch_one<Ops, 16, 4, 4, 4, EXACT, false>(p, ops, s); return true;  // config 5
+                if (variant == 7) { launch_one<Ops, 16, 4, 4, 2, EXACT, false>(p, ops, s); return true; }
+#endif
+                launch_one<Ops, 16, 4, 4, 4, EXACT, false>(p, ops, s); return true;
             }
             launch_one<Ops, 16, 4, 4, 2, EXACT, false>(p, ops, s); return true;
         case 512: launch_one<Ops, 32, 4, 4, 2, EXACT, false>(p, ops, s); return true;
@@ -167,6 +167,8 @@ bool launch_fr(const KParams& p, int d, bool exact, int variant, bool a32, cudaS
 bool launch_tdist(const KParams& p, int d, bool exact, int variant, bool a32, cudaStream_t s);
 bool launch_frattr(const KParams& p, int d, bool exact, int variant, bool a32, cudaStream_t s);
 bool launch_generic(const KParams& p, int d, bool exact, bool vectorised, cudaStream_t s);
+// d > kMaxRegDim: one warp per row, d streamed in tiles (fmm_k_stream.cu)
+bool launch_stream(const KParams& p, bool exact, cudaStream_t s);
 
 }  // namespace fmm
 

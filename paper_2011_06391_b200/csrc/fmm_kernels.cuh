@@ -32,11 +32,20 @@
 namespace fmm {
 
 constexpr int kMaxPeers = 7;  // 8 GPUs per NVSwitch domain in one process
+// Largest d the register-resident row kernels hold (masked shapes: 32 lanes
+// x 32 values); beyond it the streamed kernel (fmm_k_stream.cu) tiles d.
+constexpr int kMaxRegDim = 1024;
 
 struct PeerOut {
     float* p[kMaxPeers];
     int n;
+    const uint8_t* mask;  // per shard-local row: bit q -> peer q reads the row (nullptr: all)
 };
+
+// Peers that receive row r (bit q = zpeer[q]); all of them without a mask.
+__device__ __forceinline__ unsigned peer_bits(const uint8_t* mask, int64_t r) {
+    return mask ? static_cast<unsigned>(__ldg(mask + r)) : 0xffu;
+}
 
 struct KParams {
     const int64_t* row_ptr;  // shard-local, rebased to 0, rows+1 entries
@@ -71,6 +80,14 @@ struct KParams {
     // the per-iteration all-gather rides on the kernel's own stores
     float* zpeer[kMaxPeers];
     int n_peer;
+    // halo exchange: per shard-local row, bit q set iff peer q reads the row
+    // (one of its edges points at it); nullptr stores every row to every peer
+    const uint8_t* peer_mask;
+    // split-row fold may use float4 loads/stores: d % 4 == 0 and Z, partial
+    // and every zpeer 16-byte aligned
+    int fold_vec4;
+    // d > kMaxRegDim, scalar message: one h per edge (streamed kernel)
+    float* hbuf;
 };
 
 // ---------------------------------------------------------------- op kinds
@@ -658,21 +675,25 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
         }
         // group gg stores vectors i with i % GPW == gg; final rows (not chunk
         // partials) also go straight into the peers' next-iterate buffers
-        const bool to_peers = warp >= p.n_chunk_items;
+        const bool is_chunk = warp < p.n_chunk_items;  // a split row's partial, not a final row
+        const bool to_peers = !is_chunk && p.n_peer > 0;
+        const unsigned pm = to_peers ? peer_bits(p.peer_mask, r) : 0u;
 #pragma unroll
         for (int i = 0; i < NV; ++i)
             if ((i % GPW) == g && elem_ok[i]) {
                 store_vec<VEC>(out + (i * LPG + gl) * VEC, &z[i * VEC]);
                 if (to_peers)
                     for (int q = 0; q < p.n_peer; ++q)
-                        store_vec<VEC>(p.zpeer[q] + r * d + (i * LPG + gl) * VEC, &z[i * VEC]);
+                        if ((pm >> q) & 1u)
+                            store_vec<VEC>(p.zpeer[q] + r * d + (i * LPG + gl) * VEC, &z[i * VEC]);
             }
-        if (!to_peers && p.split_count != nullptr) {
+        if (is_chunk && p.split_count != nullptr) {
             // last chunk of the row to finish folds all its partials, in
             // chunk order per element (deterministic, shard-independent)
             const int si = p.chunks[warp].w;
             const int4 sr = p.split_rows[si];
             __threadfence();  // this warp's partial is visible device-wide
+            __syncwarp();     // ... every lane's, before lane 0 takes the ticket
             unsigned ticket = 0;
             if (lane == 0) ticket = atomicAdd(p.split_count + si, 1u);
             ticket = __shfl_sync(0xffffffffu, ticket, 0);
@@ -682,8 +703,9 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
                 float* zr = p.Z + static_cast<int64_t>(sr.x) * d;
                 const float id = aop_identity(ops);
                 const bool mx = p.fold_max != 0;
+                const unsigned fpm = p.n_peer > 0 ? peer_bits(p.peer_mask, sr.x) : 0u;
                 auto f1 = [&](float a, float v) { return mx ? (a < v ? v : a) : __fadd_rn(a, v); };
-                if ((d & 3) == 0) {
+                if (p.fold_vec4) {
                     // float4 per lane, 8 chunks in flight; per element the
                     // chunks fold in order
                     const int d4 = d >> 2;
@@ -708,14 +730,16 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
                         }
                         reinterpret_cast<float4*>(zr)[j4] = acc;
                         for (int q = 0; q < p.n_peer; ++q)
-                            reinterpret_cast<float4*>(p.zpeer[q] + static_cast<int64_t>(sr.x) * d)[j4] = acc;
+                            if ((fpm >> q) & 1u)
+                                reinterpret_cast<float4*>(p.zpeer[q] + static_cast<int64_t>(sr.x) * d)[j4] = acc;
                     }
                 } else {
                     for (int j = lane; j < d; j += 32) {
                         float acc = id;
                         for (int k = 0; k < sr.z; ++k) acc = f1(acc, __ldcg(base + static_cast<int64_t>(k) * d + j));
                         zr[j] = acc;
-                        for (int q = 0; q < p.n_peer; ++q) p.zpeer[q][static_cast<int64_t>(sr.x) * d + j] = acc;
+                        for (int q = 0; q < p.n_peer; ++q)
+                            if ((fpm >> q) & 1u) p.zpeer[q][static_cast<int64_t>(sr.x) * d + j] = acc;
                     }
                 }
                 if (lane == 0) p.split_count[si] = 0;  // ready for the next launch
@@ -782,12 +806,14 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
             }
         }
         if (active) {
+            const unsigned pm = p.n_peer > 0 ? peer_bits(p.peer_mask, r) : 0u;
 #pragma unroll
             for (int i = 0; i < NV; ++i)
                 if (elem_ok[i]) {
                     store_vec<VEC>(out + (i * LPG + gl) * VEC, &z[i * VEC]);
                     for (int q = 0; q < p.n_peer; ++q)
-                        store_vec<VEC>(p.zpeer[q] + r * d + (i * LPG + gl) * VEC, &z[i * VEC]);
+                        if ((pm >> q) & 1u)
+                            store_vec<VEC>(p.zpeer[q] + r * d + (i * LPG + gl) * VEC, &z[i * VEC]);
                 }
         }
     }
@@ -827,7 +853,9 @@ fmm_combine_kernel(const int4* __restrict__ split, const float* __restrict__ par
                 acc = is_max ? (acc < v ? v : acc) : __fadd_rn(acc, v);
             }
             zr[j] = acc;
-            for (int q = 0; q < peers.n; ++q) peers.p[q][static_cast<int64_t>(s.x) * d + j] = acc;
+            const unsigned pm = peers.n > 0 ? peer_bits(peers.mask, s.x) : 0u;
+            for (int q = 0; q < peers.n; ++q)
+                if ((pm >> q) & 1u) peers.p[q][static_cast<int64_t>(s.x) * d + j] = acc;
         }
         return;
     }
@@ -865,7 +893,9 @@ fmm_combine_kernel(const int4* __restrict__ split, const float* __restrict__ par
             acc = is_max ? (acc < v ? v : acc) : __fadd_rn(acc, v);
         }
         zr[j] = acc;
-        for (int qq = 0; qq < peers.n; ++qq) peers.p[qq][static_cast<int64_t>(s.x) * d + j] = acc;
+        const unsigned pm = peers.n > 0 ? peer_bits(peers.mask, s.x) : 0u;
+        for (int qq = 0; qq < peers.n; ++qq)
+            if ((pm >> qq) & 1u) peers.p[qq][static_cast<int64_t>(s.x) * d + j] = acc;
     }
 }
 
@@ -889,6 +919,13 @@ __global__ void fmm_narrow_cols_kernel(const int64_t* __restrict__ src, int32_t*
     local_max = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(local_max + 1))) - 1;
     if ((threadIdx.x & 31) == 0 && local_max >= 0) atomicMax(max_col, local_max);
     if (local_bad) atomicExch(bad, 1);
+}
+
+// need[c] = 1 for every column an edge points at (halo masks).
+__global__ void fmm_mark_cols_kernel(const int32_t* __restrict__ col, int64_t count, uint8_t* __restrict__ need) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        need[col[i]] = 1;
 }
 
 #endif  // FMM_AUX_KERNELS

@@ -168,61 +168,4 @@ ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t ro
     return P;
 }
 
-GroupSchedule build_group_schedule(const ShardPlan& P, int warps, int gpw, int u) {
-    GroupSchedule S;
-    S.gpw = gpw;
-    S.u = u;
-    S.warps = warps;
-    const int64_t G = static_cast<int64_t>(warps) * gpw;
-    const int64_t rows = static_cast<int64_t>(P.order.size());
-    // items in heavy-first order: chunks (row order = order prefix), then rows
-    std::vector<Int4> items;
-    items.reserve(P.chunks.size() + static_cast<size_t>(P.nonempty_rows));
-    for (const Int4& c : P.chunks) {
-        const int64_t rb = P.local_row_ptr[c.x], re = P.local_row_ptr[c.x + 1];
-        const int64_t e0 = rb + static_cast<int64_t>(c.y) * P.chunk;
-        const int64_t n = std::min<int64_t>(P.chunk, re - e0);
-        items.push_back({c.z, static_cast<int32_t>(e0), static_cast<int32_t>(n), c.x + 1});
-    }
-    for (int64_t i = P.n_split_rows; i < rows; ++i) {
-        const int32_t r = P.order[i];
-        const int64_t rb = P.local_row_ptr[r], re = P.local_row_ptr[r + 1];
-        if (re == rb) {
-            S.empty_rows.push_back(r);
-            continue;
-        }
-        items.push_back({r, static_cast<int32_t>(rb), static_cast<int32_t>(re - rb), 0});
-    }
-    // LPT: each item to the least-loaded group (ties -> lowest group id)
-    using Load = std::pair<int64_t, int64_t>;
-    std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
-    for (int64_t gi = 0; gi < G; ++gi) heap.push({0, gi});
-    std::vector<int32_t> owner(items.size());
-    std::vector<int64_t> load(static_cast<size_t>(G), 0);
-    for (size_t i = 0; i < items.size(); ++i) {
-        Load top = heap.top();
-        heap.pop();
-        const int64_t cost = (items[i].z + u - 1) / u;
-        owner[i] = static_cast<int32_t>(top.second);
-        top.first += cost;
-        load[top.second] = top.first;
-        heap.push(top);
-    }
-    // group-major item lists, assignment order kept within a group
-    S.group_item_begin.assign(static_cast<size_t>(G) + 1, 0);
-    for (size_t i = 0; i < items.size(); ++i) ++S.group_item_begin[owner[i] + 1];
-    for (int64_t gi = 0; gi < G; ++gi) S.group_item_begin[gi + 1] += S.group_item_begin[gi];
-    S.items.resize(items.size());
-    std::vector<int32_t> cursor(S.group_item_begin.begin(), S.group_item_begin.end() - 1);
-    for (size_t i = 0; i < items.size(); ++i) S.items[cursor[owner[i]]++] = items[i];
-    S.warp_steps.assign(static_cast<size_t>(warps), 0);
-    for (int64_t gi = 0; gi < G; ++gi) {
-        const int64_t w = gi / gpw;
-        S.warp_steps[w] = static_cast<int32_t>(std::max<int64_t>(S.warp_steps[w], load[gi]));
-        S.busy_group_steps += load[gi];
-    }
-    for (int32_t t : S.warp_steps) S.total_steps += t;
-    return S;
-}
-
 }  // namespace fmm

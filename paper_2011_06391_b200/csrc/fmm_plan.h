@@ -80,21 +80,4 @@ struct ShardPlan {
 
 ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t row_end, int chunk);
 
-// Per-lane-group work lists for the persistent kernel (fmm_sched.cuh).
-// Items: chunks of split rows {slot, e_begin, n, row+1} and non-empty rows
-// {row, e_begin, n, 0}; each costs ceil(n/u) steps. Items are assigned
-// longest-first to the least-loaded of warps*gpw lane groups (LPT), so the
-// groups' step counts are within one item of each other.
-struct GroupSchedule {
-    int gpw = 0, u = 0, warps = 0;
-    std::vector<int32_t> group_item_begin;  // warps*gpw + 1
-    std::vector<Int4> items;
-    std::vector<int32_t> warp_steps;        // max over the warp's groups
-    std::vector<int32_t> empty_rows;
-    int64_t total_steps = 0;                // sum of warp_steps
-    int64_t busy_group_steps = 0;           // sum over groups of their own steps
-};
-
-GroupSchedule build_group_schedule(const ShardPlan& P, int warps, int gpw, int u);
-
 }  // namespace fmm

@@ -17,8 +17,11 @@ Every fused call goes through libfusedmm_cuda's C ABI; there is no CPU path.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import enum
+import threading
+import weakref
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
 
@@ -485,8 +488,36 @@ def _vp(a: np.ndarray):
 
 
 # ----------------------------------------------------------- device objects
+# Every live native handle, so interpreter exit releases them in a defined
+# order (graphs, then contexts) while CUDA is still up, instead of leaving it
+# to finalisers that run in arbitrary order. The C ABI is itself order-safe:
+# a context outlives its graphs (fmm_destroy defers the delete).
+_live_graphs: "weakref.WeakSet" = weakref.WeakSet()
+_live_contexts: "weakref.WeakSet" = weakref.WeakSet()
+_shutting_down = False
+
+
+@atexit.register
+def _release_all() -> None:
+    global _shutting_down
+    for g in list(_live_graphs):
+        try:
+            g.free()
+        except Exception:
+            pass
+    for c in list(_live_contexts):
+        try:
+            c.close()
+        except Exception:
+            pass
+    _contexts.clear()
+    _shutting_down = True
+
+
 class Context:
-    """An fmm_ctx: one shard (CUDA stream) per entry of `devices`."""
+    """An fmm_ctx: one shard (CUDA stream) per entry of `devices`. Use as a
+    context manager or call close(); graphs uploaded on it stay valid until
+    they are freed (the native context is deleted after its last graph)."""
 
     def __init__(self, devices: Sequence[int]):
         L = _lib.lib()
@@ -497,6 +528,13 @@ class Context:
         if st != _lib.FMM_OK:
             _raise(st, None, "fmm_create failed (no CUDA device?)")
         self.h = h
+        _live_contexts.add(self)
+
+    def __enter__(self) -> "Context":
+        return self
+
+    def __exit__(self, *exc) -> None:
+        self.close()
 
     def sync(self) -> None:
         """Wait for every FMM_ASYNC call enqueued on this context."""
@@ -521,6 +559,8 @@ class Context:
             self.h = None
 
     def __del__(self):
+        if _shutting_down:
+            return
         try:
             self.close()
         except Exception:
@@ -528,6 +568,7 @@ class Context:
 
 
 _contexts: dict = {}
+_contexts_mu = threading.Lock()
 
 
 class PinnedBuffer:
@@ -561,12 +602,23 @@ def device_count() -> int:
 
 def default_context(t: int) -> Context:
     """Context with t shards over the visible GPUs (round-robin)."""
-    if t not in _contexts:
-        n = device_count()
-        if n < 1:
-            raise CudaError("no CUDA device visible (libfusedmm_cuda has no CPU fallback)")
-        _contexts[t] = Context([i % n for i in range(t)])
-    return _contexts[t]
+    with _contexts_mu:
+        if t not in _contexts:
+            n = device_count()
+            if n < 1:
+                raise CudaError("no CUDA device visible (libfusedmm_cuda has no CPU fallback)")
+            _contexts[t] = Context([i % n for i in range(t)])
+        return _contexts[t]
+
+
+def _upload_values(A: CsrMatrix):
+    """Edge values to upload: None (a_uv = 1, no value stream) when every
+    current value is exactly 1 — decided from the array at upload time, so
+    values assigned after construction are honoured."""
+    v = np.ascontiguousarray(A.values, dtype=np.float32)
+    if v.size and not np.all(v == 1.0):
+        return v
+    return None
 
 
 class DeviceGraph:
@@ -574,16 +626,46 @@ class DeviceGraph:
 
     def __init__(self, ctx: Context, A: CsrMatrix, row_begin: int = 0, row_end: Optional[int] = None):
         self.ctx = ctx
-        self.A = A
+        self.nrows, self.ncols = A.nrows, A.ncols  # no reference to A: A._device caches graphs
         rb = 0 if row_begin is None else int(row_begin)
         re = A.nrows if row_end is None else int(row_end)
         h = C.c_void_p()
-        vals = None if A.unit_values else _f32(A.values)
+        v = _upload_values(A)
         st = _lib.lib().fmm_graph_upload(ctx.h, A.nrows, A.ncols, _i64(A.row_ptr), _i64(A.col_idx),
-                                         vals, rb, re, C.byref(h))
+                                         None if v is None else _f32(v), rb, re, C.byref(h))
         _raise(st, ctx.h)
         self.h = h
         self.row_begin, self.row_end = rb, re
+        _live_graphs.add(self)
+
+    def __enter__(self) -> "DeviceGraph":
+        return self
+
+    def __exit__(self, *exc) -> None:
+        self.free()
+
+    def update_values(self, values: Optional[np.ndarray]) -> None:
+        """New a_uv for the same structure (fmm_graph_update_values); values
+        is the full nnz array of the uploaded CSR, None = all ones."""
+        v = None if values is None else np.ascontiguousarray(values, np.float32)
+        _raise(_lib.lib().fmm_graph_update_values(self.h, None if v is None else _f32(v)), self.ctx.h)
+
+    def column_use(self) -> np.ndarray:
+        """need[c] = 1 for every column this graph's edges point at."""
+        need = np.zeros(max(self.ncols, 1), np.uint8)
+        _raise(_lib.lib().fmm_graph_column_use(self.h, C.c_void_p(need.ctypes.data)), self.ctx.h)
+        return need[:self.ncols]
+
+    def set_peer_mask(self, mask: Optional[np.ndarray], npeer: int) -> None:
+        """Halo mask for fmm_run_peers: bit q of mask[r] = peer slot q reads
+        row row_begin + r (None clears it: every row to every peer)."""
+        if mask is None:
+            _raise(_lib.lib().fmm_graph_set_peer_mask(self.h, None, npeer), self.ctx.h)
+            return
+        m = np.ascontiguousarray(mask, np.uint8)
+        if m.size != self.row_end - self.row_begin:
+            raise InvalidArgument("set_peer_mask: one byte per row of the graph")
+        _raise(_lib.lib().fmm_graph_set_peer_mask(self.h, C.c_void_p(m.ctypes.data), npeer), self.ctx.h)
 
     def info(self) -> fmm_graph_info:
         I = fmm_graph_info()
@@ -646,24 +728,42 @@ class DeviceGraph:
             self.h = None
 
     def __del__(self):
+        if _shutting_down:
+            return
         try:
             self.free()
         except Exception:
             pass
 
 
+def fingerprint(a: np.ndarray) -> int:
+    """64-bit content fingerprint of an array (fmm_fingerprint)."""
+    a = np.ascontiguousarray(a)
+    return int(_lib.lib().fmm_fingerprint(C.c_void_p(a.ctypes.data), a.nbytes))
+
+
 def _device_graph(A: CsrMatrix, t: int, d: int = 0) -> DeviceGraph:
-    key = (t, A.row_ptr.ctypes.data, A.col_idx.ctypes.data, A.values.ctypes.data, A.nnz())
+    """The uploaded copy of A for t shards, keyed on A's CONTENTS: the
+    reference reads A afresh on every fused_mm (kernel.hpp:297-353), so a CSR
+    rebuilt at the same addresses, or edited in place, is re-uploaded (or,
+    when only the values changed, gets its values replaced)."""
+    skey = (t, A.nrows, A.ncols, A.nnz(), fingerprint(A.row_ptr), fingerprint(A.col_idx))
+    vals = _upload_values(A)
+    vkey = None if vals is None else fingerprint(vals)
     g = A._device.get(t)
-    if g is None or g._key != key:
-        if g is not None:
-            g.free()
-        ctx = default_context(t)
-        if t > 1:  # shards balanced on nnz + the per-row cost for this d
-            ctx.set_row_weight(row_weight_for(d) if d > 0 else 0.0)
-        g = DeviceGraph(ctx, A)
-        g._key = key
-        A._device[t] = g
+    if g is not None and g._skey == skey:
+        if g._vkey != vkey:
+            g.update_values(vals)
+            g._vkey = vkey
+        return g
+    if g is not None:
+        g.free()
+    ctx = default_context(t)
+    if t > 1:  # shards balanced on nnz + the per-row cost for this d
+        ctx.set_row_weight(row_weight_for(d) if d > 0 else 0.0)
+    g = DeviceGraph(ctx, A)
+    g._skey, g._vkey = skey, vkey
+    A._device[t] = g
     return g
 
 

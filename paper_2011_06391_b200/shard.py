@@ -37,7 +37,7 @@ ComputeFn = Callable[[torch.Tensor, torch.Tensor, int, int], torch.Tensor]
 class ShardedFusedMM:
     def __init__(self, A: CsrMatrix, d: int, spec: OpSpec, group=None,
                  device: Optional[torch.device] = None, compute: Optional[ComputeFn] = None,
-                 exchange: str = "fused"):
+                 exchange: str = "fused", halo: bool = True):
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -50,15 +50,48 @@ class ShardedFusedMM:
         if exchange not in ("fused", "broadcast"):
             raise ValueError("exchange must be 'fused' or 'broadcast'")
         self.exchange_mode = exchange if (compute is None and self.world > 1) else "broadcast"
+        self.halo = halo
+        # rows this rank stores into peers per exchange (fused mode, after
+        # the halo masks are set) and the unmasked count, for reporting
+        self.exchange_rows = (self.re - self.rb) * (self.world - 1)
+        self.exchange_rows_all = self.exchange_rows
+        self._user_compute = compute  # None: the device path (no bound method kept: no cycle)
+        self.ctx = None
+        self.graph = None
+        self._masks_set = False
         if compute is not None:
-            self._compute = compute
             self.device = device or torch.device("cpu")
         else:
             self.device = device or torch.device("cuda", torch.cuda.current_device())
             self.ctx = Context([self.device.index])
             self.ctx.set_stream(0, torch.cuda.current_stream(self.device).cuda_stream)
             self.graph = DeviceGraph(self.ctx, A, self.rb, self.re)
-            self._compute = self._device_compute
+
+    def close(self) -> None:
+        """Release the device graph and context now (do not leave it to
+        finalisers at interpreter exit)."""
+        if self.graph is not None:
+            self.graph.free()
+            self.graph = None
+        if self.ctx is not None:
+            self.ctx.close()
+            self.ctx = None
+
+    def __enter__(self) -> "ShardedFusedMM":
+        return self
+
+    def __exit__(self, *exc) -> None:
+        self.close()
+
+    def _compute(self, X: torch.Tensor, Y: torch.Tensor, rb: int, re: int,
+                 out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        if self._user_compute is not None:
+            Z = self._user_compute(X, Y, rb, re)
+            if out is not None:
+                out.copy_(Z)
+                return out
+            return Z
+        return self._device_compute(X, Y, rb, re, out)
 
     def _device_compute(self, X: torch.Tensor, Y: torch.Tensor, rb: int, re: int,
                         out: Optional[torch.Tensor] = None) -> torch.Tensor:
@@ -70,6 +103,34 @@ class ShardedFusedMM:
                               self.spec, stats=st)
         self.launches += st.launches
         return Z
+
+    def set_halo_masks(self) -> None:
+        """Per-row peer masks for the fused exchange: every rank publishes
+        which rows its edges read (fmm_graph_column_use, n bytes), and this
+        rank stores row r only to the peers that read it. Rows nobody else
+        reads — every empty row of a symmetric graph, and rows referenced
+        only from inside this block — are never sent. Collective."""
+        if self._masks_set or self.world == 1 or self.graph is None:
+            return
+        need = torch.from_numpy(self.graph.column_use()).to(self.device)
+        every = [torch.empty_like(need) for _ in range(self.world)]
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_gather(every, need, group=self.group)
+        else:
+            cpu = [torch.empty_like(need, device="cpu") for _ in range(self.world)]
+            dist.all_gather(cpu, need.cpu(), group=self.group)
+            every = cpu
+        mask = np.zeros(self.re - self.rb, np.uint8)
+        slot = 0
+        for q in range(self.world):
+            if q == self.rank:
+                continue
+            mask |= (every[q][self.rb:self.re].cpu().numpy() != 0).astype(np.uint8) << slot
+            slot += 1
+        self.graph.set_peer_mask(mask, self.world - 1)
+        info = self.graph.info()
+        self.exchange_rows, self.exchange_rows_all = int(info.exchange_rows), int(info.exchange_rows_all)
+        self._masks_set = True
 
     def step(self, X: torch.Tensor, Y: Optional[torch.Tensor] = None) -> torch.Tensor:
         """This rank's Z slice for one fused call (no collective)."""
@@ -98,45 +159,69 @@ class ShardedFusedMM:
             torch.cuda.synchronize(self.device)
             dist.barrier(group=self.group)
 
-    def _iterate_fused(self, X0: torch.Tensor, iters: int) -> torch.Tensor:
+    def map_peer_buffers(self, bufs: list) -> dict:
+        """CUDA-IPC map every peer's copies of `bufs` (same shapes on every
+        rank). Returns {peer rank: [device pointer of its bufs[i], ...]};
+        release with unmap_peer_buffers. Collective."""
         from . import fusedmm as F
-        from ._lib import fmm_stats
-        bufs = [X0.clone(), torch.empty_like(X0)]
         torch.cuda.synchronize(self.device)
         mine = [F.ipc_handle(b.data_ptr()) for b in bufs]
         every: list = [None] * self.world
         dist.all_gather_object(every, mine, group=self.group)
         dev = self.device.index
-        # (mapped base, offset) per peer buffer; the mapping is unmapped by base
-        maps: dict = {}
+        self._maps = {}
+        # both buffers of a peer may live in one caching-allocator segment
+        # (the same handle): map each distinct handle once
+        for q in range(self.world):
+            if q != self.rank:
+                self._maps[q] = {}
+                for (h, _off) in every[q]:
+                    if h not in self._maps[q]:
+                        self._maps[q][h] = F.ipc_open(h, dev)
+        return {q: [self._maps[q][h] + off for (h, off) in every[q]] for q in self._maps}
+
+    def unmap_peer_buffers(self) -> None:
+        """Collective: no rank unmaps while a peer may still store into it."""
+        from . import fusedmm as F
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        for q in getattr(self, "_maps", {}):
+            for base in self._maps[q].values():
+                F.ipc_close(base)
+        self._maps = {}
+
+    def step_exchange(self, X: torch.Tensor, nxt: torch.Tensor, peer_next: list, all_rows: bool = False) -> None:
+        """One fused call over this rank's rows of X whose z rows land in
+        nxt[rb:re] AND, over NVLink, in every peer's next buffer
+        (peer_next[q] = that buffer's device pointer on the peer, rank order
+        without self) — only the rows the peer reads unless all_rows — then
+        the stream-ordered barrier that makes every slice visible."""
+        from ._lib import FMM_ASYNC, FMM_DEVICE_PTRS, FMM_PEERS_ALL, fmm_stats
         row_off = self.rb * self.d * 4
+        targets = [p + row_off for p in peer_next]
+        st = fmm_stats()
+        flags = FMM_DEVICE_PTRS | FMM_ASYNC | (FMM_PEERS_ALL if all_rows else 0)
+        self.graph.run_device_peers(X.data_ptr(), X.shape[0], X.data_ptr(), nxt[self.rb:self.re].data_ptr(),
+                                    self.d, self.spec, targets, flags=flags, stats=st)
+        self.launches += st.launches
+        self._barrier()
+
+    def _iterate_fused(self, X0: torch.Tensor, iters: int) -> torch.Tensor:
+        if self.halo:
+            self.set_halo_masks()
+        bufs = [X0.clone(), torch.empty_like(X0)]
         try:
-            # both buffers of a peer may live in one caching-allocator
-            # segment (the same handle): map each distinct handle once
-            for q in range(self.world):
-                if q != self.rank:
-                    maps[q] = {}
-                    for (h, _off) in every[q]:
-                        if h not in maps[q]:
-                            maps[q][h] = F.ipc_open(h, dev)
-            peers = {q: [maps[q][h] + off for (h, off) in every[q]] for q in maps}
+            peers = self.map_peer_buffers(bufs)
             self._barrier()
             for it in range(iters):
                 cur, nxt = bufs[it % 2], bufs[(it + 1) % 2]
-                targets = [peers[q][(it + 1) % 2] + row_off for q in sorted(peers)]
-                st = fmm_stats()
-                self.graph.run_device_peers(cur.data_ptr(), cur.shape[0], cur.data_ptr(),
-                                            nxt[self.rb:self.re].data_ptr(), self.d, self.spec, targets,
-                                            stats=st)
-                self.launches += st.launches
-                self._barrier()  # every slice landed everywhere; nobody still reads `cur`
+                # halo rows only, except on the last iteration: the returned
+                # iterate is replicated on every rank
+                self.step_exchange(cur, nxt, [peers[q][(it + 1) % 2] for q in sorted(peers)],
+                                   all_rows=(it + 1 == iters))
             out = bufs[iters % 2]
-            torch.cuda.synchronize(self.device)
-            dist.barrier(group=self.group)  # no rank unmaps while a peer may still store into it
         finally:
-            for q in maps:
-                for base in maps[q].values():
-                    F.ipc_close(base)
+            self.unmap_peer_buffers()
         return out
 
     def iterate(self, X0: torch.Tensor, iters: int) -> torch.Tensor:
@@ -146,10 +231,7 @@ class ShardedFusedMM:
         cur = X0.clone()
         nxt = torch.empty_like(cur)
         for _ in range(iters):
-            if self._compute is self._device_compute:
-                self._device_compute(cur, cur, self.rb, self.re, out=nxt[self.rb:self.re])
-            else:
-                nxt[self.rb:self.re] = self._compute(cur, cur, self.rb, self.re)
+            self._compute(cur, cur, self.rb, self.re, out=nxt[self.rb:self.re])
             self.exchange(nxt)
             cur, nxt = nxt, cur
         return cur

@@ -76,6 +76,37 @@ int main() {
     threw = false;
     try { fc::csr_from_coo<CsrMatrix>(std::vector<Coo>{{2, 0, 1.f}}, 2, 3); } catch (const std::invalid_argument&) { threw = true; }
     CHECK(threw);
+    // the reference reads A afresh every call: values edited in place, then
+    // the whole CSR rewritten at the same addresses, are both seen
+    A.values[0] = 10.f;  // row 0: 10*y0 + 2*y1 = {14, 14}
+    DenseMatrix Zv = fc::fused_mm(A, X, Y, gcn, 1);
+    CHECK(Zv.data == (std::vector<float>{14, 14, 6, 6}));
+    A.col_idx[0] = 1;    // row 0: 10*y1 + 2*y1 = {24, 24}
+    DenseMatrix Zc = fc::fused_mm(A, X, Y, gcn, 1);
+    CHECK(Zc.data == (std::vector<float>{24, 24, 6, 6}));
+    A.col_idx[0] = 0;
+    A.values[0] = 1.f;
+    // update_u (kernel.hpp:81-107): GCN row [5,5] (test_kernel.cpp:89-96)
+    std::vector<int64_t> ucols{0, 1};
+    std::vector<float> uvals{1.f, 2.f}, xu(2, 0.f), zu(2, -1.f), scratch(4);
+    fc::update_u(ucols, uvals, xu, Y, gcn, zu, scratch);
+    CHECK(zu == (std::vector<float>{5, 5}));
+    // fused_mm_specialized (kernel.hpp:356-378) and its GENERIC rejection
+    DenseMatrix Zs = fc::fused_mm_specialized(KnownPattern::SPMM_GCN, A, X, Y, 1.f, 1);
+    CHECK(Zs.data == (std::vector<float>{5, 5, 6, 6}));
+    threw = false;
+    try { fc::fused_mm_specialized(KnownPattern::GENERIC, A, X, Y, 1.f, 1); } catch (const std::invalid_argument&) { threw = true; }
+    CHECK(threw);
+    // lane widths: 4 / 8 / 16 run, others throw; tune_lane_width picks one
+    for (int w : {4, 8, 16}) {
+        KernelOptions o{w};
+        CHECK(fc::fused_mm(A, X, Y, gcn, 1, &st, o).data == (std::vector<float>{5, 5, 6, 6}));
+    }
+    threw = false;
+    try { fc::fused_mm(A, X, Y, gcn, 1, &st, KernelOptions{3}); } catch (const std::invalid_argument&) { threw = true; }
+    CHECK(threw);
+    const int tw = fc::tune_lane_width(A, X, Y, gcn, 1, 1);
+    CHECK(tw == 4 || tw == 8);
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "wrapper ok", failures);
     return failures ? 1 : 0;
 }

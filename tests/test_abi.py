@@ -162,3 +162,39 @@ def test_part1d_weighted(seed):
                 assert r == 0 or cost[r - 1] * t < i * cost[m]
     assert L.fmm_part1d_weighted(m, row_ptr.ctypes.data_as(C.POINTER(C.c_int64)), 2, -1.0,
                                  np.zeros(3, np.int64).ctypes.data_as(C.POINTER(C.c_int64))) == _lib.FMM_E_INVAL
+
+
+REF_INCLUDE = Path("/root/reference/proj/include")
+
+
+@pytest.mark.skipif(not (REF_INCLUDE / "fusedmm" / "kernel.hpp").exists() or shutil.which("g++") is None,
+                    reason="reference headers or g++ not present")
+def test_cpp_dropin_compiles_against_reference_types():
+    """INTEGRATION.md's claim, pinned: include/fusedmm_cuda.hpp is used from
+    reference host code with the reference's own CsrMatrix / DenseMatrix /
+    OpSpec / KernelStats / KernelOptions for fused_mm, update_u,
+    fused_mm_specialized and tune_lane_width (tests/cpp/reference_dropin.cpp)."""
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", f"-I{ROOT / 'include'}",
+                        f"-I{REF_INCLUDE}", str(ROOT / "tests" / "cpp" / "reference_dropin.cpp")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
+
+
+@pytest.mark.skipif(shutil.which("g++") is None, reason="g++ not present")
+def test_cpp_wrapper_demo_builds_and_links(tmp_path):
+    """The wrapper demo compiles and links against libfusedmm_cuda (runs on
+    the GPU in test_gpu_ops.py::test_cpp_wrapper_runs)."""
+    exe = tmp_path / "demo"
+    r = subprocess.run(["g++", "-std=c++17", f"-I{ROOT / 'include'}", str(ROOT / "tests/cpp/wrapper_demo.cpp"),
+                        f"-L{_lib.LIB_PATH.parent}", "-lfusedmm_cuda", f"-Wl,-rpath,{_lib.LIB_PATH.parent}",
+                        "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
+
+
+def test_fingerprint_is_content_keyed():
+    a = np.arange(1_000_003, dtype=np.int64)
+    f0 = F.fingerprint(a)
+    assert F.fingerprint(a.copy()) == f0          # same contents, other address
+    a[777_777] += 1
+    assert F.fingerprint(a) != f0                 # same address, other contents
+    assert F.fingerprint(a[:10]) != F.fingerprint(a[:11])

@@ -35,12 +35,19 @@ def _worker(rank, world, port, cfg, iters, out, exchange="broadcast"):
         from paper_2011_06391_b200 import configs
         from paper_2011_06391_b200.shard import ShardedFusedMM
         w = configs.get(cfg, small=True)
-        sh = ShardedFusedMM(w.A, w.d, w.spec, device=torch.device("cuda", 0), exchange=exchange)
-        X0 = torch.from_numpy(w.X.array.copy()).cuda()
-        Z = sh.iterate(X0, iters)
+        # explicit lifetime: graph and context are released here, not by
+        # finalisers during interpreter shutdown
+        with ShardedFusedMM(w.A, w.d, w.spec, device=torch.device("cuda", 0), exchange=exchange) as sh:
+            X0 = torch.from_numpy(w.X.array.copy()).cuda()
+            Z = sh.iterate(X0, iters)
+            torch.cuda.synchronize()
+            if rank == 0:
+                np.save(out, Z.cpu().numpy())
+            if exchange == "fused":
+                # halo masks: rows no peer reads are never sent
+                assert sh.exchange_rows < sh.exchange_rows_all, (sh.exchange_rows, sh.exchange_rows_all)
+            del X0, Z
         torch.cuda.synchronize()
-        if rank == 0:
-            np.save(out, Z.cpu().numpy())
     finally:
         dist.destroy_process_group()
 

@@ -72,19 +72,6 @@ def test_multishard_iterate_matches_single():
     check_exact(X, Z1.array)
 
 
-@pytest.mark.parametrize("cfg", [2, 3, 5])
-@pytest.mark.parametrize("variant", ["-4", "-3"])
-def test_persistent_pipelined_kernel_parity(cfg, variant, monkeypatch):
-    """The opt-in persistent cp.async kernel (fmm_sched.cuh) against the
-    oracle, including its LPT work lists, chunk items and empty rows."""
-    monkeypatch.setenv("FMM_VARIANT", variant)
-    w = configs.get(cfg, small=True)
-    g = F.DeviceGraph(F.Context([0]), w.A)  # FMM_VARIANT is read at context creation
-    Z = np.zeros_like(w.X.array)
-    g.run_host(w.X.array, w.X.array, Z, w.d, w.spec)
-    check_tolerance(Z, oracle.oracle_fused_mm(w.A, w.X, w.X, w.spec), w.A, w.X, w.X, w.spec)
-
-
 def test_repeat_runs_bitwise_stable():
     w = configs.get(2, small=True)
     Z1 = F.fused_mm(w.A, w.X, w.X, w.spec, 1)

@@ -267,3 +267,27 @@ def test_rmat_stream_equals_reference_generator():
     rows, cols = configs.rmat_stream(9, 8, 1234)
     A = F.csr_from_coo(list(zip(rows.tolist(), cols.tolist(), [1.0] * rows.size)), 512, 512)
     assert np.array_equal(A.row_ptr, rp) and np.array_equal(A.col_idx, cl) and np.array_equal(A.values, vl)
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("cfg,scale", [(2, 13), (3, 13), (5, 12), (2, None)])
+def test_reference_arm_inputs_equal_ours_bitwise(cfg, scale):
+    """bench.py --impl reference builds its workload with the reference's own
+    generator (oracle.ref_workload: rmat_generate + the BASELINE recipe, X
+    from std::mt19937_64 blocks) so that arm loads no library of this repo;
+    the buffers are bitwise the ones our arm times (configs.py / libfmm_gen),
+    at desk scale and at config 2's full size."""
+    from paper_2011_06391_b200 import configs
+    r = oracle.ref_workload(cfg, scale=scale)
+    if scale is None:
+        w = configs.get(cfg)
+    else:
+        w = {2: lambda: configs.config2(scale=scale), 3: lambda: configs.config3(scale=scale),
+             5: lambda: configs.config5(scale=scale)}[cfg]()
+    assert np.array_equal(r.A.row_ptr, w.A.row_ptr)
+    assert np.array_equal(r.A.col_idx, w.A.col_idx)
+    assert np.array_equal(r.X.array.view(np.uint32), w.X.array.view(np.uint32))
+    assert (r.spec.vop, r.spec.rop, r.spec.sop, r.spec.mop, r.spec.aop) == \
+        (int(w.spec.vop), int(w.spec.rop), int(w.spec.sop), int(w.spec.mop), int(w.spec.aop))
+    if scale is None:
+        assert (r.name, r.description) == (w.name, w.description)
