@@ -6,11 +6,10 @@
 // order of csr_from_coo on the GPU (fmm_csr_from_coo). fmm_write_matrix_market
 // restates write_matrix_market (mmio.hpp:87-99): coordinate real general,
 // 1-based, values printed with 17 significant digits.
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <fstream>
-#include <sstream>
 #include <string>
 #include <vector>
 
@@ -31,10 +30,110 @@ struct Parsed {
     std::vector<float> vals;
 };
 
-// mmio.hpp:23-84 up to (not including) the csr_from_coo fold.
+// A cursor over one line of the file (no terminating newline). The field
+// readers follow C++ stream extraction (operator>>) exactly, because the
+// reference's error messages depend on where extraction fails: skip
+// isspace, then an integer is [+-]digits (overflow fails) and a double is
+// the longest [+-]digits[.digits][(e|E)[+-]digits] prefix, which must then
+// convert completely ("inf", "nan" and hex floats do not extract).
+struct Cursor {
+    const char* p;
+    const char* end;
+
+    void skip_space() {
+        while (p < end && (*p == ' ' || *p == '\t' || *p == '\r' || *p == '\v' || *p == '\f')) ++p;
+    }
+    bool word(std::string* out) {
+        skip_space();
+        const char* b = p;
+        while (p < end && !(*p == ' ' || *p == '\t' || *p == '\r' || *p == '\v' || *p == '\f')) ++p;
+        out->assign(b, p);
+        return p > b;
+    }
+    bool integer(int64_t* out) {
+        skip_space();
+        bool neg = false;
+        if (p < end && (*p == '+' || *p == '-')) neg = *p++ == '-';
+        if (p >= end || *p < '0' || *p > '9') return false;
+        uint64_t v = 0;
+        const uint64_t lim = neg ? uint64_t(INT64_MAX) + 1 : uint64_t(INT64_MAX);
+        for (; p < end && *p >= '0' && *p <= '9'; ++p) {
+            const uint64_t dgt = static_cast<uint64_t>(*p - '0');
+            if (v > (lim - dgt) / 10) return false;  // out of range: extraction fails
+            v = v * 10 + dgt;
+        }
+        *out = neg ? static_cast<int64_t>(0 - v) : static_cast<int64_t>(v);
+        return true;
+    }
+    bool real(double* out) {
+        skip_space();
+        std::string tok;
+        auto digits = [&] {
+            size_t k = 0;
+            for (; p < end && *p >= '0' && *p <= '9'; ++p, ++k) tok.push_back(*p);
+            return k;
+        };
+        if (p < end && (*p == '+' || *p == '-')) tok.push_back(*p++);
+        size_t mant = digits();
+        if (p < end && *p == '.') {
+            tok.push_back(*p++);
+            mant += digits();
+        }
+        if (mant == 0) return false;
+        if (p < end && (*p == 'e' || *p == 'E')) {
+            tok.push_back(*p++);
+            if (p < end && (*p == '+' || *p == '-')) tok.push_back(*p++);
+            if (digits() == 0) return false;  // "1e": the collected token does not convert
+        }
+        char* stop = nullptr;
+        const double v = std::strtod(tok.c_str(), &stop);
+        // overflow fails (the stream reports +-max with failbit); underflow
+        // to a subnormal or zero is accepted, as by libstdc++'s num_get
+        if (*stop != '\0' || v == HUGE_VAL || v == -HUGE_VAL) return false;
+        *out = v;
+        return true;
+    }
+};
+
+// The file as lines, numbered from 1 like std::getline: a final line
+// without a newline counts, nothing after the last newline does.
+class LineReader {
+public:
+    explicit LineReader(std::string text) : buf_(std::move(text)) {}
+    bool next(Cursor* c) {
+        if (pos_ >= buf_.size()) return false;
+        const size_t nl = buf_.find('\n', pos_);
+        const size_t stop = nl == std::string::npos ? buf_.size() : nl;
+        c->p = buf_.data() + pos_;
+        c->end = buf_.data() + stop;
+        pos_ = nl == std::string::npos ? buf_.size() : nl + 1;
+        ++lineno_;
+        return true;
+    }
+    long lineno() const { return lineno_; }
+
+private:
+    std::string buf_;
+    size_t pos_ = 0;
+    long lineno_ = 0;
+};
+
+bool slurp(const std::string& path, std::string* out) {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) return false;
+    char chunk[1 << 16];
+    size_t k;
+    while ((k = std::fread(chunk, 1, sizeof(chunk), f)) > 0) out->append(chunk, k);
+    std::fclose(f);
+    return true;
+}
+
+// Header, comment, size-line and entry rules of read_matrix_market
+// (mmio.hpp:23-84) and its "<path>:<line>: <what>" messages; the duplicate
+// fold (csr_from_coo) runs afterwards on the GPU.
 bool parse(const std::string& path, Parsed* P, std::string* msg) {
-    std::ifstream in(path);
-    if (!in) {
+    std::string text;
+    if (!slurp(path, &text)) {
         *msg = "cannot open " + path;
         return false;
     }
@@ -42,59 +141,62 @@ bool parse(const std::string& path, Parsed* P, std::string* msg) {
         *msg = path + ":" + std::to_string(line) + ": " + what;
         return false;
     };
-    std::string line;
-    long lineno = 0;
-    if (!std::getline(in, line)) return fail(1, "empty file");
-    ++lineno;
-    std::istringstream hdr(line);
-    std::string banner, object, format, field, symmetry;
-    hdr >> banner >> object >> format >> field >> symmetry;
-    if (banner != "%%MatrixMarket" || object != "matrix" || format != "coordinate")
+    LineReader lines(std::move(text));
+    Cursor cur{};
+    if (!lines.next(&cur)) return fail(1, "empty file");
+    std::string tok[5];  // banner, object, format, field, symmetry ("" when absent)
+    for (std::string& t : tok) cur.word(&t);
+    if (tok[0] != "%%MatrixMarket" || tok[1] != "matrix" || tok[2] != "coordinate")
         return fail(1, "malformed MatrixMarket header");
-    if (field != "real" && field != "pattern" && field != "integer")
-        return fail(1, "unsupported field type '" + field + "'");
-    if (symmetry != "general" && symmetry != "symmetric")
-        return fail(1, "unsupported symmetry '" + symmetry + "'");
+    const std::string& field = tok[3];
+    const std::string& symmetry = tok[4];
     const bool pattern = field == "pattern";
+    if (!pattern && field != "real" && field != "integer")
+        return fail(1, "unsupported field type '" + field + "'");
     const bool symmetric = symmetry == "symmetric";
-    int64_t m = 0, n = 0, declared = 0;
-    while (std::getline(in, line)) {
-        ++lineno;
-        if (line.empty() || line[0] == '%') continue;
-        std::istringstream sz(line);
-        if (!(sz >> m >> n >> declared)) return fail(lineno, "malformed size line");
+    if (!symmetric && symmetry != "general") return fail(1, "unsupported symmetry '" + symmetry + "'");
+    auto is_skipped = [](const Cursor& c) { return c.p == c.end || *c.p == '%'; };
+
+    int64_t dims[3] = {0, 0, 0};  // m, n, declared entries
+    while (lines.next(&cur)) {
+        if (is_skipped(cur)) continue;
+        // a failed extraction leaves the earlier fields read (m, n may be set)
+        int64_t v[3] = {0, 0, 0};
+        int k = 0;
+        while (k < 3 && cur.integer(&v[k])) dims[k] = v[k], ++k;
+        if (k < 3) return fail(lines.lineno(), "malformed size line");
         break;
     }
-    if (m <= 0 || n < 0) return fail(lineno, "invalid matrix dimensions");
+    const int64_t m = dims[0], n = dims[1], declared = dims[2];
+    if (m <= 0 || n < 0) return fail(lines.lineno(), "invalid matrix dimensions");
     P->m = m;
     P->n = n;
-    const size_t reserve = static_cast<size_t>(std::max<int64_t>(declared, 0)) * (symmetric ? 2 : 1);
-    P->rows.reserve(reserve);
-    P->cols.reserve(reserve);
-    P->vals.reserve(reserve);
+    const size_t cap = static_cast<size_t>(std::max<int64_t>(declared, 0)) * (symmetric ? 2 : 1);
+    P->rows.reserve(cap);
+    P->cols.reserve(cap);
+    P->vals.reserve(cap);
     int64_t seen = 0;
-    while (std::getline(in, line)) {
-        ++lineno;
-        if (line.empty() || line[0] == '%') continue;
-        std::istringstream es(line);
-        int64_t r, c;
-        if (!(es >> r >> c)) return fail(lineno, "malformed entry");
+    while (lines.next(&cur)) {
+        if (is_skipped(cur)) continue;
+        int64_t r = 0, c = 0;
+        if (!cur.integer(&r) || !cur.integer(&c)) return fail(lines.lineno(), "malformed entry");
         double v = 1.0;
-        if (!pattern && !(es >> v)) return fail(lineno, "non-numeric value");
-        if (r < 1 || r > m || c < 1 || c > n) return fail(lineno, "index out of declared bounds");
+        if (!pattern && !cur.real(&v)) return fail(lines.lineno(), "non-numeric value");
+        if (r < 1 || r > m || c < 1 || c > n) return fail(lines.lineno(), "index out of declared bounds");
+        const float fv = static_cast<float>(v);
         P->rows.push_back(r - 1);
         P->cols.push_back(c - 1);
-        P->vals.push_back(static_cast<float>(v));
-        if (symmetric && r != c) {
+        P->vals.push_back(fv);
+        if (symmetric && r != c) {  // mirrored off-diagonal entry
             P->rows.push_back(c - 1);
             P->cols.push_back(r - 1);
-            P->vals.push_back(static_cast<float>(v));
+            P->vals.push_back(fv);
         }
         ++seen;
     }
     if (seen != declared)
-        return fail(lineno, "entry count " + std::to_string(seen) + " does not match declared " +
-                                std::to_string(declared));
+        return fail(lines.lineno(), "entry count " + std::to_string(seen) + " does not match declared " +
+                                        std::to_string(declared));
     return true;
 }
 

@@ -131,6 +131,11 @@ MM_CASES = {
     "symmetric_pattern": "%%MatrixMarket matrix coordinate pattern symmetric\n4 4 4\n2 1\n3 1\n4 4\n3 1\n",
     "integer": "%%MatrixMarket matrix coordinate integer general\n2 2 2\n1 1 3\n2 2 -4\n",
     "empty": "%%MatrixMarket matrix coordinate real general\n5 5 0\n",
+    # stream-extraction corner cases the reference accepts
+    "crlf": "%%MatrixMarket matrix coordinate real general\r\n2 3 2\r\n1 3 0.5\r\n2 1 -2\r\n",
+    "signs_tabs": "%%MatrixMarket  matrix\tcoordinate real general extra\n2 2 2\n+1\t+2 +2.5\n2 2 -.5\n",
+    "value_prefixes": "%%MatrixMarket matrix coordinate real general\n3 3 4\n1 1 1.5abc\n2 2 0x1p3\n3 3 5.\n1 3 1e-310\n",
+    "no_final_newline": "%%MatrixMarket matrix coordinate pattern general\n2 2 1\n2 1",
 }
 MM_BAD = {
     "header": "%%MatrixMarket matrix array real general\n2 2 0\n",
@@ -143,6 +148,23 @@ MM_BAD = {
     "bounds": "%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 1.0\n",
     "count": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n",
     "empty_file": "",
+    # stream-extraction corner cases the reference rejects
+    "inf_value": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 inf\n",
+    "nan_value": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 nan\n",
+    "exp_no_digits": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 1e\n",
+    "exp_overflow": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 -1e999\n",
+    "dot_value": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 .\n",
+    "int_overflow": "%%MatrixMarket matrix coordinate real general\n2 2 1\n99999999999999999999 1 1.0\n",
+    "float_index": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1.0 1 1.0\n",
+    "spaced_comment": "%%MatrixMarket matrix coordinate real general\n2 2 1\n % not a comment\n1 1 1\n",
+    "crlf_blank": "%%MatrixMarket matrix coordinate real general\r\n\r\n2 2 0\r\n",
+    "header_short": "%%MatrixMarket matrix coordinate\n2 2 0\n",
+    "header_case": "%%matrixmarket matrix coordinate real general\n2 2 0\n",
+    "size_missing": "%%MatrixMarket matrix coordinate real general\n% only comments\n",
+    "size_float": "%%MatrixMarket matrix coordinate real general\n2.0 2 1\n",
+    "neg_dims": "%%MatrixMarket matrix coordinate real general\n2 -1 0\n",
+    "count_no_newline": "%%MatrixMarket matrix coordinate real general\n2 2 3\n1 1 1\n2 2 2",
+    "count_over": "%%MatrixMarket matrix coordinate pattern symmetric\n2 2 1\n1 2\n2 1\n",
 }
 
 
