@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "fusedmm/apps.hpp"
+#include "fusedmm/bench.hpp"
 #include "fusedmm/kernel.hpp"
 #include "fusedmm/mmio.hpp"
 #include "fusedmm/matrix.hpp"
@@ -284,6 +285,54 @@ int fmm_ref_pattern_of(const RefSpec* s) {
 //    Box-Muller on pairs (u1, u2): sqrt(-2 ln(1-u1)) * (cos, sin)(2 pi u2);
 //    U(lo,hi) = lo + (hi-lo)*u01.
 void fmm_ref_free(void* p) { std::free(p); }
+
+// write_csv (bench.hpp:175-190) of n records given as POD fields, for
+// pinning the device bench's CSV format byte for byte.
+struct RefRecord {
+    const char* graph;
+    const char* app;
+    int64_t m, n, nnz, d;
+    double avg_degree;
+    int32_t threads, iterations;
+    double fused_seconds, reference_seconds, speedup, achieved_gflops, ai_lower_bound;
+    uint64_t fused_aux_bytes, materialized_h_bytes;
+    int32_t reference_oom, verified;
+};
+
+int fmm_ref_write_csv(const char* path, int count, const RefRecord* recs) {
+    try {
+        std::vector<BenchRecord> v;
+        for (int i = 0; i < count; ++i) {
+            const RefRecord& q = recs[i];
+            BenchRecord r;
+            r.graph = q.graph;
+            r.m = q.m;
+            r.n = q.n;
+            r.nnz = q.nnz;
+            r.avg_degree = q.avg_degree;
+            r.d = q.d;
+            r.app = q.app;
+            r.threads = q.threads;
+            r.iterations = q.iterations;
+            r.fused_seconds = q.fused_seconds;
+            r.reference_seconds = q.reference_seconds;
+            r.speedup = q.speedup;
+            r.achieved_gflops = q.achieved_gflops;
+            r.ai_lower_bound = q.ai_lower_bound;
+            r.fused_aux_bytes = q.fused_aux_bytes;
+            r.materialized_h_bytes = q.materialized_h_bytes;
+            r.reference_oom = q.reference_oom != 0;
+            r.verified = q.verified != 0;
+            v.push_back(r);
+        }
+        write_csv(v, std::string(path));
+        return 0;
+    } catch (...) {
+        return 1;
+    }
+}
+
+double fmm_ref_arithmetic_intensity(double avg_degree, int64_t d) { return arithmetic_intensity(avg_degree, d); }
 
 int fmm_ref_rmat_sym(int scale, int edge_factor, double a, double b, double c, uint64_t seed, int64_t** row_ptr,
                      int64_t** col, int64_t* nnz) {
