@@ -317,6 +317,29 @@ fmm_status fmm_csr_sym_unique(int device, int64_t n, int64_t count,
                               int drop_self, int symmetrize, int64_t* row_ptr,
                               int64_t* col_idx, int64_t* nnz_out);
 
+/* rmat_generate (rmat.hpp:24-61) on GPU `device`: the seeded insertion
+ * stream (scale levels of quadrant descent per edge from one mt19937_64)
+ * generated on the device by independent sub-streams whose generator states
+ * come from a jump-ahead (fmm_mt64_window), bitwise the reference's sequential
+ * stream; then
+ *   recipe 0: csr_from_coo of the stream (= rmat_generate: self-loops kept,
+ *             duplicates summed into values; col_idx / values with room for
+ *             edge_factor << scale entries),
+ *   recipe 1: the BASELINE.json recipe (fmm_csr_sym_unique: self-loops
+ *             dropped, symmetrised, sorted, unique; col_idx with room for
+ *             2 * edge_factor << scale; values unused),
+ *   recipe 2: the raw stream into rows_out / cols_out (edge_factor << scale).
+ * row_ptr has scale-sized n + 1 entries; *nnz_out = entries written. */
+fmm_status fmm_rmat_device(int device, int scale, int edge_factor, double a,
+                           double b, double c, uint64_t seed, int recipe,
+                           int64_t* row_ptr, int64_t* col_idx, float* values,
+                           int64_t* rows_out, int64_t* cols_out,
+                           int64_t* nnz_out);
+/* The 312-word window (x_p .. x_{p+311}) of std::mt19937_64(seed)'s word
+ * recurrence: its next outputs are temper(x_{p+312}), ... i.e. outputs
+ * p, p+1, ... of the generator (host; polynomial jump-ahead). */
+fmm_status fmm_mt64_window(uint64_t seed, uint64_t position, uint64_t* window);
+
 #ifdef __cplusplus
 }
 #endif

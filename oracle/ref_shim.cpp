@@ -286,6 +286,13 @@ int fmm_ref_pattern_of(const RefSpec* s) {
 //    U(lo,hi) = lo + (hi-lo)*u01.
 void fmm_ref_free(void* p) { std::free(p); }
 
+// outputs skip .. skip+count-1 of std::mt19937_64(seed) (jump-ahead pin)
+void fmm_ref_mt64_outputs(uint64_t seed, uint64_t skip, int64_t count, uint64_t* out) {
+    std::mt19937_64 g(seed);
+    g.discard(skip);
+    for (int64_t i = 0; i < count; ++i) out[i] = g();
+}
+
 // write_csv (bench.hpp:175-190) of n records given as POD fields, for
 // pinning the device bench's CSV format byte for byte.
 struct RefRecord {

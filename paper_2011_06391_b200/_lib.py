@@ -97,6 +97,9 @@ SIGNATURES = {
     "fmm_free": (None, [_P]),
     "fmm_csr_sym_unique": (C.c_int, [C.c_int, C.c_int64, C.c_int64, _I64P, _I64P, C.c_int, C.c_int,
                                      _I64P, _I64P, _I64P]),
+    "fmm_rmat_device": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_uint64,
+                                  C.c_int, _I64P, _I64P, _FP, _I64P, _I64P, _I64P]),
+    "fmm_mt64_window": (C.c_int, [C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64)]),
 }
 
 _lib = None

@@ -38,7 +38,7 @@ CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-march=x86-64-v3", f"-I{INCLUDE}", f
 CUDA_SOURCES = ["fmm_api.cu", "fmm_k_sigmoid.cu", "fmm_k_gcn.cu", "fmm_k_fr.cu",
                 "fmm_k_tdist.cu", "fmm_k_frattr.cu", "fmm_k_generic.cu", "fmm_k_stream.cu", "fmm_unfused.cu",
                 "fmm_ingest.cu"]
-HOST_SOURCES = ["fmm_plan.cpp", "fmm_mmio.cpp"]
+HOST_SOURCES = ["fmm_plan.cpp", "fmm_mmio.cpp", "fmm_mt64.cpp"]
 
 
 def _newest_dep() -> float:

@@ -10,7 +10,9 @@ the CPU oracle while keeping each config's shape and value distribution.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
+from typing import Optional
 
 import numpy as np
 
@@ -80,6 +82,41 @@ def rmat_generate(scale: int, edge_factor: int = 16, seed: int = 1, device: int 
     return csr_from_coo_device(rows, cols, None, n, n, device)
 
 
+def rmat_device(scale: int, edge_factor: int, seed: int, recipe: int = 1, device: int = 0):
+    """The R-MAT graphs built entirely on the GPU (fmm_rmat_device): the
+    insertion stream from jump-ahead mt19937_64 sub-streams, then recipe 1
+    (BASELINE: drop self-loops, symmetrise, sort, unique — equals rmat_sym),
+    recipe 0 (csr_from_coo: equals the reference's rmat_generate), or
+    recipe 2 (the raw stream as (rows, cols))."""
+    from .fusedmm import InvalidArgument, _raise
+    n = 1 << scale
+    ne = edge_factor << scale
+    L = _lib.lib()
+    P64 = C.POINTER(C.c_int64)
+    nnz = C.c_int64()
+    if recipe == 2:
+        rows = np.zeros(max(ne, 1), np.int64)
+        cols = np.zeros(max(ne, 1), np.int64)
+        st = L.fmm_rmat_device(device, scale, edge_factor, *RMAT_ABC, seed, 2, None, None, None,
+                               rows.ctypes.data_as(P64), cols.ctypes.data_as(P64), C.byref(nnz))
+        if st == _lib.FMM_E_INVAL:
+            raise InvalidArgument("rmat_device: bad parameters")
+        _raise(st)
+        return rows[:ne], cols[:ne]
+    rp = np.zeros(n + 1, np.int64)
+    cap = max((2 if recipe == 1 else 1) * ne, 1)
+    cl = np.zeros(cap, np.int64)
+    vl = np.zeros(cap, np.float32) if recipe == 0 else None
+    st = L.fmm_rmat_device(device, scale, edge_factor, *RMAT_ABC, seed, recipe, rp.ctypes.data_as(P64),
+                           cl.ctypes.data_as(P64), None if vl is None else vl.ctypes.data_as(C.POINTER(C.c_float)),
+                           None, None, C.byref(nnz))
+    if st == _lib.FMM_E_INVAL:
+        raise InvalidArgument("rmat_device: bad parameters")
+    _raise(st)
+    k = nnz.value
+    return CsrMatrix(n, n, rp, cl[:k].copy(), None if vl is None else vl[:k].copy())
+
+
 def rmat_stream(scale: int, edge_factor: int, seed: int):
     """Raw insertion stream (rows, cols) for cross-checks with the reference."""
     ne = edge_factor << scale
@@ -121,17 +158,28 @@ def config1(n: int = 16384, k: int = 16, d: int = 64, seed: int = 0) -> Workload
                     f"ER n={n} k={k} d={d} GCN SpMM, seed {seed}")
 
 
-def config2(scale: int = 20, edge_factor: int = 16, d: int = 128, seed: int = 1) -> Workload:
+def _rmat_graph(scale: int, edge_factor: int, seed: int, gen: Optional[str]) -> CsrMatrix:
+    """BASELINE R-MAT graph from the host builder ("host") or wholly on the
+    GPU ("device", fmm_rmat_device); both are the same CSR (tested). The
+    default follows FMM_GEN (host when unset)."""
+    gen = gen or os.environ.get("FMM_GEN", "host")
+    if gen == "device":
+        return rmat_device(scale, edge_factor, seed, recipe=1)
+    return rmat_sym(scale, edge_factor, seed)
+
+
+def config2(scale: int = 20, edge_factor: int = 16, d: int = 128, seed: int = 1, gen: Optional[str] = None) -> Workload:
     """R-MAT sigmoid embedding; X ~ 0.1 N(0,1)."""
-    A = rmat_sym(scale, edge_factor, seed)
+    A = _rmat_graph(scale, edge_factor, seed, gen)
     X = DenseMatrix.wrap(normal_fill(A.nrows * d, 0.1, seed).reshape(A.nrows, d))
     return Workload("config2_sigmoid", A, X, make_spec(App.NODE_EMBED_SIGMOID), 1, False, False,
                     f"R-MAT scale {scale} ef {edge_factor} d={d} sigmoid embedding, seed {seed}")
 
 
-def config3(scale: int = 21, edge_factor: int = 8, d: int = 32, seed: int = 2, iters: int = 20) -> Workload:
+def config3(scale: int = 21, edge_factor: int = 8, d: int = 32, seed: int = 2, iters: int = 20,
+            gen: Optional[str] = None) -> Workload:
     """R-MAT t-distribution layout; X ~ U(-10,10); 20 iterations X <- Z."""
-    A = rmat_sym(scale, edge_factor, seed)
+    A = _rmat_graph(scale, edge_factor, seed, gen)
     X = DenseMatrix.wrap(uniform_fill(A.nrows * d, -10.0, 10.0, seed).reshape(A.nrows, d))
     return Workload("config3_tdist", A, X, tdist_spec(), iters, False, False,
                     f"R-MAT scale {scale} ef {edge_factor} d={d} t-distribution, {iters} iterations, seed {seed}")
@@ -155,9 +203,10 @@ def config4(side: int = 2048, seed: int = 3, k: float = 1.0) -> Workload:
                     False, True, f"{side}x{side} lattice + shortcut, d=2 FR-attractive k={k}, seed {seed}")
 
 
-def config5(scale: int = 24, edge_factor: int = 32, d: int = 256, seed: int = 4, iters: int = 5) -> Workload:
+def config5(scale: int = 24, edge_factor: int = 32, d: int = 256, seed: int = 4, iters: int = 5,
+            gen: Optional[str] = None) -> Workload:
     """Large R-MAT sigmoid embedding, 5 epochs X <- Z."""
-    A = rmat_sym(scale, edge_factor, seed)
+    A = _rmat_graph(scale, edge_factor, seed, gen)
     X = DenseMatrix.wrap(normal_fill(A.nrows * d, 0.1, seed).reshape(A.nrows, d))
     return Workload("config5_sigmoid_large", A, X, make_spec(App.NODE_EMBED_SIGMOID), iters, False, False,
                     f"R-MAT scale {scale} ef {edge_factor} d={d} sigmoid, {iters} epochs, seed {seed}")

@@ -19,11 +19,14 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cmath>
+#include <numeric>
 #include <cstdint>
 #include <cstring>
 #include <string>
 #include <vector>
 
+#include "fmm_mt64.h"
 #include "fusedmm_cuda.h"
 
 namespace {
@@ -169,32 +172,121 @@ fmm_status counts_to_row_ptr(Scratch& S, unsigned long long* counts, int64_t m, 
     return FMM_OK;
 }
 
-}  // namespace
+// ---- the R-MAT insertion stream on the device (rmat.hpp:32-58) ----------
+// One warp per sub-stream of E edges (E*scale words, a multiple of 312): the
+// sub-stream's mt19937_64 window comes from the host jump-ahead
+// (fmm_mt64.cpp); the warp twists 312 words at a time (two phases: words
+// 0..155 depend only on the old window, 156..311 also on the new 0..155),
+// tempers them, and descends `scale` quadrant levels per edge from its
+// consecutive words. u01 < t is evaluated exactly as (r >> 11) < ceil(t*2^53)
+// (u01 = (r >> 11) * 2^-53 is exact in double), so the stream is bitwise the
+// reference's sequential one.
+constexpr int kMtN = 312, kMtM = 156;
+constexpr int kGenWarps = 4;
 
-extern "C" {
+__device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
+    y ^= (y >> 29) & 0x5555555555555555ull;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+    y ^= (y << 37) & 0xFFF7EEE000000000ull;
+    y ^= y >> 43;
+    return y;
+}
+__device__ __forceinline__ uint64_t mt_next(uint64_t x0, uint64_t x1, uint64_t xm) {
+    const uint64_t y = (x0 & 0xFFFFFFFF80000000ull) | (x1 & 0x7FFFFFFFull);
+    return xm ^ (y >> 1) ^ ((x1 & 1) ? 0xB5026F5AA96619E9ull : 0ull);
+}
 
-fmm_status fmm_csr_from_coo(int device, int64_t m, int64_t n, int64_t count, const int64_t* rows,
-                            const int64_t* cols, const float* vals, int64_t* row_ptr, int64_t* col_idx,
+__global__ void __launch_bounds__(32 * kGenWarps)
+rmat_stream_kernel(const uint64_t* __restrict__ windows, int64_t nstreams, int64_t edges_per_stream, int64_t nedges,
+                   int scale, uint64_t ta, uint64_t tab, uint64_t tabc, int64_t* __restrict__ rows,
+                   int64_t* __restrict__ cols) {
+    __shared__ uint64_t raw[kGenWarps][2][kMtN];   // window, next window
+    __shared__ uint64_t tmp[kGenWarps][2][kMtN];   // tempered words of the last two chunks
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int64_t sid = static_cast<int64_t>(blockIdx.x) * kGenWarps + wl;
+    if (sid >= nstreams) return;
+    const int64_t e_begin = sid * edges_per_stream;
+    const int64_t e_end = min(nedges, e_begin + edges_per_stream);
+    for (int i = lane; i < kMtN; i += 32) raw[wl][0][i] = windows[sid * kMtN + i];
+    __syncwarp();
+    int cur = 0;
+    int64_t chunk = 0, e = e_begin;
+    while (e < e_end) {
+        const uint64_t* o = raw[wl][cur];
+        uint64_t* nw = raw[wl][cur ^ 1];
+        for (int i = lane; i < kMtM; i += 32) nw[i] = mt_next(o[i], o[i + 1], o[i + kMtM]);
+        __syncwarp();
+        for (int i = kMtM + lane; i < kMtN; i += 32)
+            nw[i] = mt_next(o[i], i + 1 < kMtN ? o[i + 1] : nw[0], nw[i - kMtM]);
+        __syncwarp();
+        uint64_t* tw = tmp[wl][chunk & 1];
+        for (int i = lane; i < kMtN; i += 32) tw[i] = mt_temper(nw[i]);
+        __syncwarp();
+        cur ^= 1;
+        // edges whose words all lie in chunks <= this one
+        const int64_t words_avail = (chunk + 1) * kMtN;
+        const int64_t e_lim = min(e_end, e_begin + words_avail / scale);
+        for (int64_t eb = e; eb < e_lim; eb += 32) {
+            const int64_t ee = eb + lane;
+            if (ee < e_lim) {
+                int64_t w = (ee - e_begin) * scale;
+                uint64_t row = 0, col = 0;
+                for (int level = 0; level < scale; ++level, ++w) {
+                    const uint64_t k = tmp[wl][(w / kMtN) & 1][w % kMtN] >> 11;
+                    row <<= 1;
+                    col <<= 1;
+                    if (k < ta) {
+                    } else if (k < tab) {
+                        col |= 1;
+                    } else if (k < tabc) {
+                        row |= 1;
+                    } else {
+                        row |= 1;
+                        col |= 1;
+                    }
+                }
+                rows[ee] = static_cast<int64_t>(row);
+                cols[ee] = static_cast<int64_t>(col);
+            }
+        }
+        e = e_lim;
+        ++chunk;
+        __syncwarp();
+    }
+}
+
+// rows/cols[0..nedges) = the stream of rmat_generate(scale, nedges/2^scale,
+// a, b, c, seed) (device arrays)
+fmm_status rmat_stream_dev(cudaStream_t st, Scratch& S, int scale, int64_t nedges, double a, double b, double c,
+                           uint64_t seed, int64_t* d_rows, int64_t* d_cols) {
+    if (nedges == 0) return FMM_OK;
+    // sub-stream length: E edges, E*scale a multiple of 312 words
+    int64_t unit = kMtN / std::gcd<int64_t>(kMtN, scale);
+    const int64_t target = std::max<int64_t>(1, nedges / 2048);
+    const int64_t E = ((target + unit - 1) / unit) * unit;
+    const int64_t nstreams = (nedges + E - 1) / E;
+    const std::vector<uint64_t> win = fmm::mt64::windows(seed, static_cast<uint64_t>(E * scale), nstreams);
+    uint64_t* d_win;
+    ING_CK(S.alloc(&d_win, win.size()));
+    ING_CK(cudaMemcpyAsync(d_win, win.data(), win.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    auto thr = [](double t) { return static_cast<uint64_t>(std::ceil(t * 0x1.0p53)); };
+    const uint64_t ta = thr(a), tab = thr(a + b), tabc = thr(a + b + c);
+    const unsigned blocks = static_cast<unsigned>((nstreams + kGenWarps - 1) / kGenWarps);
+    rmat_stream_kernel<<<blocks, 32 * kGenWarps, 0, st>>>(d_win, nstreams, E, nedges, scale, ta, tab, tabc, d_rows,
+                                                           d_cols);
+    ING_CK(cudaGetLastError());
+    ING_CK(cudaStreamSynchronize(st));  // win (host vector) is released on return
+    return FMM_OK;
+}
+
+// csr_from_coo over device arrays d_rows / d_cols / d_vals (nullable),
+// results copied to the host arrays. Caller set the device.
+fmm_status csr_from_coo_dev(cudaStream_t st, Scratch& S, int64_t m, int64_t n, int64_t count, const int64_t* d_rows,
+                            const int64_t* d_cols, const float* d_vals, int64_t* row_ptr, int64_t* col_idx,
                             float* values, int64_t* nnz_out) {
-    if (m < 0 || n < 0 || count < 0 || !row_ptr || !nnz_out) return FMM_E_INVAL;
-    if (count > 0 && (!rows || !cols || !col_idx)) return FMM_E_INVAL;
-    if (m >= (int64_t(1) << 32) || n > INT32_MAX || count > UINT32_MAX) return FMM_E_UNSUPPORTED;
-    *nnz_out = 0;
-    if (cudaSetDevice(device) != cudaSuccess) return status_of(cudaErrorInvalidDevice);
-    cudaStream_t st;
-    ING_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    struct StreamGuard {
-        cudaStream_t s;
-        ~StreamGuard() { cudaStreamDestroy(s); }
-    } guard{st};
-    Scratch S;
-    int64_t *d_rows, *d_cols;
-    float* d_vals = nullptr;
     uint64_t *keys, *keys_s;
     uint32_t *idx, *idx_s;
     int* bad;
-    ING_CK(S.alloc(&d_rows, count));
-    ING_CK(S.alloc(&d_cols, count));
     ING_CK(S.alloc(&keys, count));
     ING_CK(S.alloc(&keys_s, count));
     ING_CK(S.alloc(&idx, count));
@@ -202,12 +294,6 @@ fmm_status fmm_csr_from_coo(int device, int64_t m, int64_t n, int64_t count, con
     ING_CK(S.alloc(&bad, 1));
     ING_CK(cudaMemsetAsync(bad, 0, sizeof(int), st));
     if (count > 0) {
-        ING_CK(cudaMemcpyAsync(d_rows, rows, count * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-        ING_CK(cudaMemcpyAsync(d_cols, cols, count * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-        if (vals) {
-            ING_CK(S.alloc(&d_vals, count));
-            ING_CK(cudaMemcpyAsync(d_vals, vals, count * sizeof(float), cudaMemcpyHostToDevice, st));
-        }
         coo_keys_kernel<<<grid_for(count), kThreads, 0, st>>>(d_rows, d_cols, count, m, n, keys, idx, bad);
         ING_CK(cudaGetLastError());
     }
@@ -279,34 +365,18 @@ fmm_status fmm_csr_from_coo(int device, int64_t m, int64_t n, int64_t count, con
     return FMM_OK;
 }
 
-fmm_status fmm_csr_sym_unique(int device, int64_t n, int64_t count, const int64_t* rows, const int64_t* cols,
-                              int drop_self, int symmetrize, int64_t* row_ptr, int64_t* col_idx,
-                              int64_t* nnz_out) {
-    if (n < 0 || count < 0 || !row_ptr || !nnz_out) return FMM_E_INVAL;
-    if (count > 0 && (!rows || !cols || !col_idx)) return FMM_E_INVAL;
-    if (n > INT32_MAX || 2 * count > static_cast<int64_t>(UINT32_MAX)) return FMM_E_UNSUPPORTED;
-    *nnz_out = 0;
-    if (cudaSetDevice(device) != cudaSuccess) return status_of(cudaErrorInvalidDevice);
-    cudaStream_t st;
-    ING_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    struct StreamGuard {
-        cudaStream_t s;
-        ~StreamGuard() { cudaStreamDestroy(s); }
-    } guard{st};
-    Scratch S;
+// the BASELINE recipe over device arrays (see fmm_csr_sym_unique)
+fmm_status sym_unique_dev(cudaStream_t st, Scratch& S, int64_t n, int64_t count, const int64_t* d_rows,
+                          const int64_t* d_cols, int drop_self, int symmetrize, int64_t* row_ptr, int64_t* col_idx,
+                          int64_t* nnz_out) {
     const int64_t nk = 2 * count;
-    int64_t *d_rows, *d_cols;
     uint64_t *keys, *keys_s;
     int* bad;
-    ING_CK(S.alloc(&d_rows, count));
-    ING_CK(S.alloc(&d_cols, count));
     ING_CK(S.alloc(&keys, nk));
     ING_CK(S.alloc(&keys_s, nk));
     ING_CK(S.alloc(&bad, 1));
     ING_CK(cudaMemsetAsync(bad, 0, sizeof(int), st));
     if (count > 0) {
-        ING_CK(cudaMemcpyAsync(d_rows, rows, count * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-        ING_CK(cudaMemcpyAsync(d_cols, cols, count * sizeof(int64_t), cudaMemcpyHostToDevice, st));
         sym_keys_kernel<<<grid_for(count), kThreads, 0, st>>>(d_rows, d_cols, count, n, drop_self, symmetrize, keys,
                                                                bad);
         ING_CK(cudaGetLastError());
@@ -353,6 +423,97 @@ fmm_status fmm_csr_sym_unique(int device, int64_t n, int64_t count, const int64_
     ING_CK(cudaStreamSynchronize(st));
     *nnz_out = U;
     return FMM_OK;
+}
+
+struct StreamGuard {
+    cudaStream_t s = nullptr;
+    ~StreamGuard() {
+        if (s) cudaStreamDestroy(s);
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+fmm_status fmm_csr_from_coo(int device, int64_t m, int64_t n, int64_t count, const int64_t* rows,
+                            const int64_t* cols, const float* vals, int64_t* row_ptr, int64_t* col_idx,
+                            float* values, int64_t* nnz_out) {
+    if (m < 0 || n < 0 || count < 0 || !row_ptr || !nnz_out) return FMM_E_INVAL;
+    if (count > 0 && (!rows || !cols || !col_idx)) return FMM_E_INVAL;
+    if (m >= (int64_t(1) << 32) || n > INT32_MAX || count > UINT32_MAX) return FMM_E_UNSUPPORTED;
+    *nnz_out = 0;
+    if (cudaSetDevice(device) != cudaSuccess) return status_of(cudaErrorInvalidDevice);
+    StreamGuard g;
+    ING_CK(cudaStreamCreateWithFlags(&g.s, cudaStreamNonBlocking));
+    Scratch S;
+    int64_t *d_rows, *d_cols;
+    float* d_vals = nullptr;
+    ING_CK(S.alloc(&d_rows, count));
+    ING_CK(S.alloc(&d_cols, count));
+    if (count > 0) {
+        ING_CK(cudaMemcpyAsync(d_rows, rows, count * sizeof(int64_t), cudaMemcpyHostToDevice, g.s));
+        ING_CK(cudaMemcpyAsync(d_cols, cols, count * sizeof(int64_t), cudaMemcpyHostToDevice, g.s));
+        if (vals) {
+            ING_CK(S.alloc(&d_vals, count));
+            ING_CK(cudaMemcpyAsync(d_vals, vals, count * sizeof(float), cudaMemcpyHostToDevice, g.s));
+        }
+    }
+    return csr_from_coo_dev(g.s, S, m, n, count, d_rows, d_cols, d_vals, row_ptr, col_idx, values, nnz_out);
+}
+
+fmm_status fmm_csr_sym_unique(int device, int64_t n, int64_t count, const int64_t* rows, const int64_t* cols,
+                              int drop_self, int symmetrize, int64_t* row_ptr, int64_t* col_idx,
+                              int64_t* nnz_out) {
+    if (n < 0 || count < 0 || !row_ptr || !nnz_out) return FMM_E_INVAL;
+    if (count > 0 && (!rows || !cols || !col_idx)) return FMM_E_INVAL;
+    if (n > INT32_MAX || 2 * count > static_cast<int64_t>(UINT32_MAX)) return FMM_E_UNSUPPORTED;
+    *nnz_out = 0;
+    if (cudaSetDevice(device) != cudaSuccess) return status_of(cudaErrorInvalidDevice);
+    StreamGuard g;
+    ING_CK(cudaStreamCreateWithFlags(&g.s, cudaStreamNonBlocking));
+    Scratch S;
+    int64_t *d_rows, *d_cols;
+    ING_CK(S.alloc(&d_rows, count));
+    ING_CK(S.alloc(&d_cols, count));
+    if (count > 0) {
+        ING_CK(cudaMemcpyAsync(d_rows, rows, count * sizeof(int64_t), cudaMemcpyHostToDevice, g.s));
+        ING_CK(cudaMemcpyAsync(d_cols, cols, count * sizeof(int64_t), cudaMemcpyHostToDevice, g.s));
+    }
+    return sym_unique_dev(g.s, S, n, count, d_rows, d_cols, drop_self, symmetrize, row_ptr, col_idx, nnz_out);
+}
+
+fmm_status fmm_rmat_device(int device, int scale, int edge_factor, double a, double b, double c, uint64_t seed,
+                           int recipe, int64_t* row_ptr, int64_t* col_idx, float* values, int64_t* rows_out,
+                           int64_t* cols_out, int64_t* nnz_out) {
+    if (scale < 1 || scale > 30 || edge_factor < 0 || !nnz_out || recipe < 0 || recipe > 2) return FMM_E_INVAL;
+    if (!(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0 + 1e-12)) return FMM_E_INVAL;
+    const int64_t nverts = int64_t(1) << scale;
+    const int64_t nedges = static_cast<int64_t>(edge_factor) * nverts;
+    if (recipe != 2 && (!row_ptr || (nedges > 0 && !col_idx))) return FMM_E_INVAL;
+    if (recipe == 2 && (!rows_out || !cols_out)) return FMM_E_INVAL;
+    if (nedges > static_cast<int64_t>(UINT32_MAX) / 2) return FMM_E_UNSUPPORTED;
+    *nnz_out = 0;
+    if (cudaSetDevice(device) != cudaSuccess) return status_of(cudaErrorInvalidDevice);
+    StreamGuard g;
+    ING_CK(cudaStreamCreateWithFlags(&g.s, cudaStreamNonBlocking));
+    Scratch S;
+    int64_t *d_rows, *d_cols;
+    ING_CK(S.alloc(&d_rows, nedges));
+    ING_CK(S.alloc(&d_cols, nedges));
+    const fmm_status gs = rmat_stream_dev(g.s, S, scale, nedges, a, b, c, seed, d_rows, d_cols);
+    if (gs != FMM_OK) return gs;
+    if (recipe == 2) {  // the raw insertion stream
+        ING_CK(cudaMemcpyAsync(rows_out, d_rows, nedges * sizeof(int64_t), cudaMemcpyDeviceToHost, g.s));
+        ING_CK(cudaMemcpyAsync(cols_out, d_cols, nedges * sizeof(int64_t), cudaMemcpyDeviceToHost, g.s));
+        ING_CK(cudaStreamSynchronize(g.s));
+        *nnz_out = nedges;
+        return FMM_OK;
+    }
+    if (recipe == 0)  // rmat_generate: csr_from_coo of the stream, unit values summed
+        return csr_from_coo_dev(g.s, S, nverts, nverts, nedges, d_rows, d_cols, nullptr, row_ptr, col_idx, values,
+                                nnz_out);
+    return sym_unique_dev(g.s, S, nverts, nedges, d_rows, d_cols, 1, 1, row_ptr, col_idx, nnz_out);
 }
 
 }  // extern "C"

@@ -268,3 +268,76 @@ def test_ref_io_rmat_size_contract_and_determinism():
     assert A.nrows == 1024 and 0 < A.nnz() <= 8192 and F.validate(A) is None
     B = configs.rmat_generate(10, 8, 5)
     same_csr((A.row_ptr, A.col_idx, A.values), (B.row_ptr, B.col_idx, B.values))
+
+
+# ------------------------------------------- device R-MAT (jump-ahead MT64)
+def _mt64_outputs_from_window(w: np.ndarray, count: int) -> np.ndarray:
+    """Next `count` outputs of the word recurrence from a 312-word window
+    (numpy restatement of the twist + tempering, test-side)."""
+    A, UM, LM = np.uint64(0xB5026F5AA96619E9), np.uint64(0xFFFFFFFF80000000), np.uint64(0x7FFFFFFF)
+    out = []
+    x = w.astype(np.uint64).copy()
+    while sum(o.size for o in out) < count:
+        nw = np.zeros(312, np.uint64)
+
+        def nxt(x0, x1, xm):
+            y = (x0 & UM) | (x1 & LM)
+            return xm ^ (y >> np.uint64(1)) ^ np.where((x1 & np.uint64(1)) != 0, A, np.uint64(0))
+        nw[:156] = nxt(x[:156], x[1:157], x[156:312])
+        nw[156:311] = nxt(x[156:311], x[157:312], nw[0:155])
+        nw[311] = nxt(x[311:312], nw[0:1], nw[155:156])[0]
+        y = nw.copy()
+        y ^= (y >> np.uint64(29)) & np.uint64(0x5555555555555555)
+        y ^= (y << np.uint64(17)) & np.uint64(0x71D67FFFEDA60000)
+        y ^= (y << np.uint64(37)) & np.uint64(0xFFF7EEE000000000)
+        y ^= y >> np.uint64(43)
+        out.append(y)
+        x = nw
+    return np.concatenate(out)[:count]
+
+
+@needs_ref
+@pytest.mark.parametrize("seed,pos", [(1, 0), (1, 1), (4, 311), (4, 312), (2, 123457), (7, 10 ** 9 + 7),
+                                      (1, 24 * 32 * (1 << 24) - 624)])
+def test_mt64_jump_ahead_equals_std_mt19937_64(seed, pos):
+    """fmm_mt64_window(seed, p): the polynomial jump-ahead gives the window
+    whose next outputs are std::mt19937_64(seed) outputs p, p+1, ... — up to
+    config 5's last sub-stream (scale 24 x 32 edges x 24 words)."""
+    import ctypes as C
+    from paper_2011_06391_b200 import _lib
+    w = np.zeros(312, np.uint64)
+    assert _lib.lib().fmm_mt64_window(seed, pos, w.ctypes.data_as(C.POINTER(C.c_uint64))) == 0
+    want = np.zeros(700, np.uint64)
+    L = oracle.ref_lib()
+    L.fmm_ref_mt64_outputs.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.POINTER(C.c_uint64)]
+    L.fmm_ref_mt64_outputs(seed, pos, want.size, want.ctypes.data_as(C.POINTER(C.c_uint64)))
+    assert np.array_equal(_mt64_outputs_from_window(w, want.size), want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scale,ef,seed", [(10, 16, 1), (13, 8, 2), (12, 32, 4), (7, 3, 9)])
+def test_device_rmat_stream_equals_host_stream(scale, ef, seed):
+    """The raw insertion stream generated on the device (jump-ahead
+    sub-streams) equals the sequential host stream (pinned to the
+    reference's rmat_generate by test_oracle.py)."""
+    r_d, c_d = configs.rmat_device(scale, ef, seed, recipe=2)
+    r_h, c_h = configs.rmat_stream(scale, ef, seed)
+    assert np.array_equal(r_d, r_h) and np.array_equal(c_d, c_h)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scale,ef,seed", [(9, 16, 1), (12, 8, 5)])
+def test_device_rmat_generate_recipe_equals_reference(scale, ef, seed):
+    A = configs.rmat_device(scale, ef, seed, recipe=0)
+    if oracle.ref_available():
+        same_csr((A.row_ptr, A.col_idx, A.values), oracle.ref_rmat(scale, ef, seed))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scale,ef,seed", [(13, 16, 1), (20, 16, 1)])
+def test_device_rmat_baseline_recipe_equals_host_builder(scale, ef, seed):
+    """The BASELINE graph built wholly on the device equals the host builder
+    (config 2 at its full size included)."""
+    A = configs.rmat_device(scale, ef, seed, recipe=1)
+    B = configs.rmat_sym(scale, ef, seed)
+    assert np.array_equal(A.row_ptr, B.row_ptr) and np.array_equal(A.col_idx, B.col_idx)
