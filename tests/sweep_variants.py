@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--variants", default="-1,0,1,2,3,4")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--small", action="store_true")
+    ap.add_argument("--env", default="", help="NAME=v1,v2,...: sweep an environment variable too")
     ap.add_argument("--exact", action="store_true")
     ap.add_argument("--hot", type=int, default=0,
                     help="characterisation: remap every column to col %% HOT (an L2-resident gather set)")
@@ -53,8 +54,11 @@ def main():
     nnzd = A.nnz() * d
     flags = _lib.FMM_DEVICE_PTRS | _lib.FMM_ASYNC | (_lib.FMM_EXACT if a.exact else 0)
     out = []
-    for v in [int(s) for s in a.variants.split(",")]:
+    env_name, env_vals = (a.env.split("=", 1)[0], a.env.split("=", 1)[1].split(",")) if a.env else ("", [""])
+    for v, ev in [(int(s), e) for s in a.variants.split(",") for e in env_vals]:
         os.environ["FMM_VARIANT"] = str(v)
+        if env_name:
+            os.environ[env_name] = ev
         ctx = F.Context([0])
         ctx.set_stream(0, stream.cuda_stream)
         g = F.DeviceGraph(ctx, A)
@@ -85,7 +89,7 @@ def main():
             except AssertionError as e:
                 par = f"FAIL {e}"
         ms = float(np.median(times))
-        rec = {"config": a.config, "variant": v, "median_ms": ms, "min_ms": float(min(times)),
+        rec = {"config": a.config, "variant": v, "env": f"{env_name}={ev}" if env_name else "", "median_ms": ms, "min_ms": float(min(times)),
                "nnzd_per_s": nnzd / (ms / 1e3), "alg_GBps": w.alg_bytes() / (ms / 1e3) / 1e9, "parity": par}
         print(json.dumps(rec), flush=True)
         out.append(rec)
