@@ -282,8 +282,10 @@ def run_ours(args):
         dist.all_reduce(tot)
         mx = sent.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        barrier = "a host barrier (gloo, ranks sharing one GPU: test mode)" if share else \
+            "a stream-ordered NCCL barrier"
         exchange = {"how": "in-kernel P2P stores (CUDA IPC over NVLink) of each z row into the next-iterate "
-                           "buffer of every peer that reads it, then a stream-ordered NCCL barrier",
+                           f"buffer of every peer that reads it, then {barrier}",
                     "bytes_per_step_total": int(tot[0].item()), "bytes_per_step_max_rank": int(mx[0].item()),
                     "bytes_per_step_without_halo_masks": int(tot[1].item()),
                     "cut_by_masks": 1.0 - float(tot[0].item()) / max(float(tot[1].item()), 1.0)}

@@ -7,6 +7,7 @@ TAG=${1:-r01}
 OUT=gpurun_out
 mkdir -p $OUT
 BENCH="python bench.py --steps 3 --warmup 3 --no-cpu"
+export FMM_GEN=device  # R-MAT graphs built on the GPU (same CSR as the host builder)
 # 1) plain run of the exact command that ncu will wrap (must exit 0 first)
 $BENCH > $OUT/${TAG}_plain.log 2>&1 || { echo "plain bench failed"; exit 1; }
 # 2) launch list: every kernel of the bench command with its device time
@@ -16,7 +17,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 ncu --set full --clock-control none --import-source on -k regex:fmm_rows -s 3 -c 1 \
     -o $OUT/${TAG}_config2_rows $BENCH > $OUT/${TAG}_ncu_c2.log 2>&1
 # 4) the other configs' kernels through the sweep tool
-for c in 3 4 1; do
+for c in 3 4 1 5; do
   python tests/sweep_variants.py --config $c --variants=-1 --iters 3 > $OUT/${TAG}_plain_c$c.log 2>&1 &&
   ncu --set full --clock-control none --import-source on -k regex:fmm_rows -s 3 -c 1 \
       -o $OUT/${TAG}_config${c}_rows python tests/sweep_variants.py --config $c --variants=-1 --iters 3 \
