@@ -377,15 +377,18 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
         return fmm::launch_stream(p, exact, stream) ? 1 : -1;
     }
     const size_t a = static_cast<size_t>(d) * sizeof(float);
-    const bool a16 = (d % 4 == 0) && aligned(X, 16) && aligned(Y, 16) && aligned(Z, 16) &&
-                     (partial == nullptr || aligned(partial, 16)) && (a % 16 == 0);
-    const bool a8 = (d % 2 == 0) && aligned(X, 8) && aligned(Y, 8) && aligned(Z, 8) &&
-                    (partial == nullptr || aligned(partial, 8));
+    bool a16 = (d % 4 == 0) && aligned(X, 16) && aligned(Y, 16) && aligned(Z, 16) &&
+               (partial == nullptr || aligned(partial, 16)) && (a % 16 == 0);
+    bool a8 = (d % 2 == 0) && aligned(X, 8) && aligned(Y, 8) && aligned(Z, 8) &&
+              (partial == nullptr || aligned(partial, 8));
     bool a32 = (d % 8 == 0) && aligned(X, 32) && aligned(Y, 32) && aligned(Z, 32) &&
                (partial == nullptr || aligned(partial, 32));
     bool fold4 = (d % 4 == 0) && aligned(Z, 16) && (partial == nullptr || aligned(partial, 16));
+    // the vector shapes also store z rows to the peers with the same width
     for (int q = 0; q < po.n; ++q) {
         a32 = a32 && aligned(po.p[q], 32);
+        a16 = a16 && aligned(po.p[q], 16);
+        a8 = a8 && aligned(po.p[q], 8);
         fold4 = fold4 && aligned(po.p[q], 16);
     }
     p.fold_vec4 = fold4 ? 1 : 0;

@@ -192,3 +192,23 @@ def test_iterate_halo_masks_cut_exchange(cfg):
     # symmetric graph: an empty row has no in-edges, nobody reads it
     assert info.exchange_rows <= info.exchange_rows_all - 2 * empty
     assert info.exchange_rows < info.exchange_rows_all
+
+
+def test_unaligned_peer_buffer_falls_back_to_masked_shapes():
+    """peer buffers that are not 16/32-byte aligned must not be
+    stored with vector stores; the call picks the masked shapes and the peer
+    receives exactly the rows Z receives."""
+    import torch
+    w = configs.get(2, small=True)
+    dev = torch.device("cuda", 0)
+    with F.Context([0]) as ctx:
+        g = F.DeviceGraph(ctx, w.A)
+        X = torch.from_numpy(w.X.array.copy()).to(dev)
+        Z = torch.zeros_like(X)
+        peer = torch.zeros(X.numel() + 1, dtype=torch.float32, device=dev)
+        g.run_device_peers(X.data_ptr(), X.shape[0], X.data_ptr(), Z.data_ptr(), w.d, w.spec,
+                           [peer.data_ptr() + 4], flags=_lib.FMM_DEVICE_PTRS)
+        torch.cuda.synchronize()
+        check_exact(peer[1:].view(X.shape).cpu().numpy(), Z.cpu().numpy())
+        check_tolerance(Z.cpu().numpy(), oracle.oracle_fused_mm(w.A, w.X, w.X, w.spec), w.A, w.X, w.X, w.spec)
+        g.free()
