@@ -134,3 +134,26 @@ def test_bulk_mt19937_64_matches_std():
     G.fmmgen_mt64_check.argtypes = [C.c_uint64, C.c_int64]
     for seed in (0, 1, 4, 5489, 2**63 + 7):
         assert G.fmmgen_mt64_check(seed, 300_000) == 0
+
+
+def test_parity_rejects_non_finite_mismatch():
+    """a NaN (or a finite/non-finite mismatch) in a GPU row must
+    fail the tolerance gate; identical non-finite values (the AMAX identity
+    -inf of an empty row) must not."""
+    from tests.parity import check_tolerance
+    A = F.CsrMatrix(3, 3, np.array([0, 1, 1, 2]), np.array([1, 0]), None)
+    X = F.DenseMatrix(3, 2, np.ones(6, np.float32))
+    spec = F.OpSpec(F.Vop.MUL, F.Rop.NOOP, F.Sop.NOOP, F.Mop.MUL, F.Aop.AMAX)
+    Zr = oracle.oracle_fused_mm(A, X, X, spec)
+    assert np.isneginf(Zr[1]).all()  # empty row: the AMAX identity
+    check_tolerance(Zr.copy(), Zr, A, X, X, spec)  # identical incl. -inf: passes
+    bad = Zr.copy()
+    bad[0, 1] = np.nan
+    with pytest.raises(AssertionError):
+        check_tolerance(bad, Zr, A, X, X, spec)
+    bad = Zr.copy()
+    bad[1, 0] = 0.0  # finite where the oracle has -inf
+    with pytest.raises(AssertionError):
+        check_tolerance(bad, Zr, A, X, X, spec)
+    e = oracle.row_errors(np.array([[np.nan, 1.0]]), np.array([[np.nan, 1.0]]))
+    assert e[0] == 0.0
