@@ -9,13 +9,15 @@ workloads. Metric: nnz*d/s (whole job).
 
 ours:      one step = one fused call over every rank's row block (part1d
            balanced on nnz plus a per-row cost; rows never split) with the
-           inputs resident in HBM; with N > 1 the step also carries the Z
-           exchange of an iterative epoch: every finished z row is stored by
-           the kernel itself, over NVLink (CUDA IPC), into the next-iterate
-           buffer of each peer that reads it (halo masks), and a
-           stream-ordered barrier closes the step. X is held fixed across
-           steps, so every step moves the same bytes (an X <- Z feedback would
-           move exactly these). Device time: CUDA events on the launch stream,
+           inputs resident in HBM. For the iterative workloads (--config 3 /
+           5) with N > 1 the step also carries the epoch's Z exchange: every
+           finished z row is stored by the kernel itself, over NVLink (CUDA
+           IPC), into the next-iterate buffer of each peer that reads it
+           (halo masks), and a stream-ordered barrier closes the step; X is
+           held fixed across steps, so every step moves the same bytes (an
+           X <- Z feedback would move exactly these). Config 2 is one call:
+           Z stays row-sharded, and the halo bytes an iteration would move
+           are reported beside the line. Device time: CUDA events on the launch stream,
            max over ranks; L2 flushed (256 MiB write) between timed steps
            outside the events. e2e: the same call through the C ABI with
            pinned HOST buffers (X host->device, Z device->host in the timed
@@ -266,10 +268,29 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     st = _lib.fmm_stats()
     exchange = None
+    iterative = w.iters > 1  # configs 3 and 5: X <- Z between iterations / epochs
     if world > 1:
+        sh.set_halo_masks()
+    if world > 1 and not iterative:
+        # config 2 is ONE fused call (BASELINE.json): each rank writes its row
+        # block of Z, as the reference's workers write disjoint row ranges of
+        # one Z (kernel.hpp:335-345); no exchange belongs to the call. The
+        # halo bytes an iterated embedding would move are reported beside it.
+        Z_dev = torch.empty((re - rb, d), dtype=torch.float32, device=dev)
+
+        def step():
+            g.run_device(X_dev.data_ptr(), m, X_dev.data_ptr(), Z_dev.data_ptr(), d, spec, stats=st)
+        sent = torch.tensor([sh.exchange_rows * d * 4, sh.exchange_rows_all * d * 4], dtype=torch.float64,
+                            device=dev)
+        tot = sent.clone()
+        dist.all_reduce(tot)
+        exchange = {"in_step": False,
+                    "why": "single-call workload: Z stays row-sharded (no collective on the data path)",
+                    "halo_bytes_per_iteration_if_iterated": int(tot[0].item()),
+                    "all_rows_bytes_per_iteration": int(tot[1].item())}
+    elif world > 1:
         # the epoch's Z exchange, fused into the kernel: z rows go straight
         # into each reading peer's next-iterate buffer (halo masks)
-        sh.set_halo_masks()
         nxt = torch.empty_like(X_dev)
         peers = sh.map_peer_buffers([nxt])
         peer_next = [peers[q][0] for q in sorted(peers)]
@@ -284,7 +305,8 @@ def run_ours(args):
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         barrier = "a host barrier (gloo, ranks sharing one GPU: test mode)" if share else \
             "a stream-ordered NCCL barrier"
-        exchange = {"how": "in-kernel P2P stores (CUDA IPC over NVLink) of each z row into the next-iterate "
+        exchange = {"in_step": True,
+                    "how": "in-kernel P2P stores (CUDA IPC over NVLink) of each z row into the next-iterate "
                            f"buffer of every peer that reads it, then {barrier}",
                     "bytes_per_step_total": int(tot[0].item()), "bytes_per_step_max_rank": int(mx[0].item()),
                     "bytes_per_step_without_halo_masks": int(tot[1].item()),
@@ -299,7 +321,8 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    launches_per_step = (sh.launches - launches0) // max(args.warmup, 1) if world > 1 else int(st.launches)
+    launches_per_step = ((sh.launches - launches0) // max(args.warmup, 1) if (world > 1 and iterative)
+                         else int(st.launches))
 
     # ---- timed region: K steps, L2 flushed between steps outside the events
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -404,7 +427,7 @@ def run_ours(args):
         cpu = {"value": nnzd_s / sec, "unit": "nnz*d/s", "cores": threads, "kind": kind,
                "sample": f"{sample} x{len(times)} (1 warm-up), all host threads"}
 
-    if world > 1:
+    if world > 1 and iterative:
         sh.unmap_peer_buffers()
     g_e.free()
     ctx_e.close()
@@ -423,7 +446,7 @@ def run_ours(args):
                         "split_rows": int(info.split_rows), "max_degree": int(info.max_degree),
                         "gen_seconds": round(gen_s, 2),
                         "step": ("fused call + halo exchange of the epoch's Z (X fixed across steps)"
-                                 if world > 1 else "one fused call")},
+                                 if (world > 1 and iterative) else "one fused call")},
             "exchange": exchange,
             "roofline": roofline,
             "e2e": {"value": e2e_value, "unit": "nnz*d/s", "h2d_bytes_per_step": int(m * d * 4),

@@ -69,14 +69,23 @@ def test_sharded_device_iterate_ranks(tmp_path, cfg, iters, world, exchange):
     check_exact(np.load(out), ref.array)
 
 
-def test_bench_torchrun_two_ranks_shared_gpu():
-    env = dict(os.environ, FMM_BENCH_SHARE_GPU="1")
+@pytest.mark.parametrize("config", [2, 3])
+def test_bench_torchrun_two_ranks_shared_gpu(config):
+    """bench.py under torchrun: config 2 (one call, Z row-sharded) and config
+    3 (iterative: the step carries the halo exchange, fused into the kernel)."""
+    env = dict(os.environ, FMM_BENCH_SHARE_GPU="1", FMM_GEN="device")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(ROOT / "bench.py"),
-           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu"]
-    r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600)
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu", "--config", str(config)]
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1
     rec = json.loads(lines[0])
     assert rec["n_gpus"] == 2 and rec["value"] > 0 and rec["gpu_launches"] > 0
+    ex = rec["exchange"]
+    if config == 3:
+        assert ex["in_step"] and ex["cut_by_masks"] > 0.38
+        assert ex["bytes_per_step_total"] < ex["bytes_per_step_without_halo_masks"]
+    else:
+        assert not ex["in_step"] and ex["halo_bytes_per_iteration_if_iterated"] > 0
