@@ -569,6 +569,7 @@ class Context:
 
 _contexts: dict = {}
 _contexts_mu = threading.Lock()
+_call_mu = threading.RLock()  # fused_mm / iterate: graph-cache lookup + run
 
 
 class PinnedBuffer:
@@ -805,21 +806,24 @@ def fused_mm(A: CsrMatrix, X: DenseMatrix, Y: DenseMatrix, spec: OpSpec, t: int 
         if stats is not None:
             stats.threads, stats.pattern = t, pattern_of(spec)
         return Z
-    g = _device_graph(A, t, X.dim)
     Xd = X.data if X.data.size else np.zeros(1, np.float32)
     Yd = Y.data if Y.data.size else np.zeros(1, np.float32)
     s = fmm_stats()
     prev = None
-    if opts is not None and opts.variant is not None:
-        prev = g.ctx.variant()
-        g.ctx.set_variant(opts.variant)
-    try:
-        st = _lib.lib().fmm_run(g.ctx.h, g.h, C.byref(spec.to_c()), X.dim, _vp(Xd), Y.nrows,
-                                _vp(Xd) if Y is X else _vp(Yd), _vp(Z.data), flags, C.byref(s))
-    finally:
-        if prev is not None:
-            g.ctx.set_variant(prev)
-    _raise(st, g.ctx.h)
+    # lookup + run under one lock: another thread's call on the same A must
+    # not replace (free) the cached graph between the two
+    with _call_mu:
+        g = _device_graph(A, t, X.dim)
+        if opts is not None and opts.variant is not None:
+            prev = g.ctx.variant()
+            g.ctx.set_variant(opts.variant)
+        try:
+            st = _lib.lib().fmm_run(g.ctx.h, g.h, C.byref(spec.to_c()), X.dim, _vp(Xd), Y.nrows,
+                                    _vp(Xd) if Y is X else _vp(Yd), _vp(Z.data), flags, C.byref(s))
+        finally:
+            if prev is not None:
+                g.ctx.set_variant(prev)
+        _raise(st, g.ctx.h)
     if stats is not None:
         stats.fill(s)
     return Z
@@ -879,8 +883,9 @@ def iterate(A: CsrMatrix, X: DenseMatrix, spec: OpSpec, iters: int, t: int = 1,
     out = DenseMatrix.wrap(X.array.copy())
     if A.nrows == 0:
         return out
-    g = _device_graph(A, t, X.dim)
-    s = g.iterate_host(out.data, X.dim, spec, iters, _flags(opts))
+    with _call_mu:
+        g = _device_graph(A, t, X.dim)
+        s = g.iterate_host(out.data, X.dim, spec, iters, _flags(opts))
     if stats is not None:
         stats.fill(s)
     return out

@@ -212,3 +212,32 @@ def test_unaligned_peer_buffer_falls_back_to_masked_shapes():
         check_exact(peer[1:].view(X.shape).cpu().numpy(), Z.cpu().numpy())
         check_tolerance(Z.cpu().numpy(), oracle.oracle_fused_mm(w.A, w.X, w.X, w.spec), w.A, w.X, w.X, w.spec)
         g.free()
+
+
+def test_concurrent_host_threads_share_the_api():
+    """Several host threads calling fused_mm on shared and private graphs:
+    every result equals the oracle (the cached graph is never freed under a
+    running call: lookup and run hold one lock, the C context a mutex)."""
+    import threading
+    shared = _rand_graph(50, 200, 200, 10)
+    X = F.DenseMatrix(200, 64, np.random.default_rng(51).uniform(-1, 1, 200 * 64))
+    spec = F.make_spec(F.App.GCN_FORWARD)
+    want_shared = oracle.oracle_fused_mm(shared, X, X, spec)
+    errors = []
+
+    def worker(k):
+        try:
+            own = _rand_graph(60 + k, 200, 200, 6 + k)
+            want_own = oracle.oracle_fused_mm(own, X, X, spec)
+            for _ in range(8):
+                check_exact(F.fused_mm(shared, X, X, spec).array, want_shared)
+                check_exact(F.fused_mm(own, X, X, spec).array, want_own)
+        except Exception as e:  # noqa: BLE001 - surfaced below
+            errors.append(e)
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors[0]
