@@ -60,6 +60,13 @@ def test_fullsize_config3_twenty_iterations_teacher_forced(cfg_cache):
     # the device-resident loop (X <- Z on the device) reproduces the chain
     Zi = F.iterate(w.A, w.X, w.spec, w.iters, 1)
     check_exact(Zi.array, X.array)
+    # ... and so do 3 shards exchanging only their halo rows (fused peer
+    # stores with per-row peer masks), bitwise, at full size
+    g3 = F._device_graph(w.A, 3, w.d)
+    Z3 = F.iterate(w.A, w.X, w.spec, w.iters, 3)
+    check_exact(Z3.array, X.array)
+    I = g3.info()
+    assert I.exchange_rows < 0.5 * I.exchange_rows_all
 
 
 def test_config5_sampled_rows():
