@@ -79,7 +79,26 @@ def main():
              4: configs.config4(side=16), 5: configs.config5(scale=7)}
     for c, w in small.items():
         save(f"config{c}_desk", w.A, w.X, w.X, w.spec)
+    large_d(specs)
+
+
+def large_d(specs=None):
+    """d past the device's register-resident shapes (1024): the streamed
+    kernel's cases (own seed, so the files above are unchanged)."""
+    rng = np.random.default_rng(1100)
+    specs = specs or {"sigmoid": F.make_spec(F.App.NODE_EMBED_SIGMOID), "gcn": F.make_spec(F.App.GCN_FORWARD),
+                      "fr": F.make_spec(F.App.FR_LAYOUT, F.AppParams(alpha=0.5)), "tdist": F.tdist_spec(),
+                      "vecmsg_sigmoid_amax": F.OpSpec(F.Vop.MUL, F.Rop.NOOP, F.Sop.SIGMOID, F.Mop.MUL,
+                                                      F.Aop.AMAX)}
+    for name in ("sigmoid", "gcn", "fr", "tdist", "vecmsg_sigmoid_amax"):
+        A, X, Y = random_case(rng, 14, 12, 1100, 0.3)
+        X = F.DenseMatrix(14, 1100, X.array * 0.05)
+        Y = F.DenseMatrix(12, 1100, Y.array * 0.05)
+        save(f"rand_{name}_d1100", A, X, Y, specs[name])
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["--large-d"]:
+        large_d()
+    else:
+        main()
