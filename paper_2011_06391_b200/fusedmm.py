@@ -465,13 +465,19 @@ class KernelStats:
 
 @dataclass
 class KernelOptions:
-    """kernel.hpp:286-288. lane_width is the CPU lane-blocking width; on the
-    device it is validated for interface parity; the device's own shape
-    choice is `variant` (None = the context's, -1 = default for d; see
-    tune_lane_width). exact: None = per-pattern default, True/False = force."""
+    """kernel.hpp:286-288. lane_width (4, 8 or 16, as in the reference)
+    selects the device's gather width like the C++ wrapper does: 4 -> the
+    128-bit-load shapes (variant 20), 8 / 16 -> the default 256-bit shapes;
+    `variant` (tuning: any dispatcher shape id) overrides it.
+    exact: None = per-pattern default, True/False = force the scheme."""
     lane_width: int = 8
     exact: Optional[bool] = None
     variant: Optional[int] = None
+
+    def device_variant(self) -> Optional[int]:
+        if self.variant is not None:
+            return self.variant
+        return 20 if self.lane_width == 4 else None
 
 
 # ------------------------------------------------------------ ctypes utils
@@ -810,13 +816,14 @@ def fused_mm(A: CsrMatrix, X: DenseMatrix, Y: DenseMatrix, spec: OpSpec, t: int 
     Yd = Y.data if Y.data.size else np.zeros(1, np.float32)
     s = fmm_stats()
     prev = None
+    want = opts.device_variant() if opts is not None else None
     # lookup + run under one lock: another thread's call on the same A must
     # not replace (free) the cached graph between the two
     with _call_mu:
         g = _device_graph(A, t, X.dim)
-        if opts is not None and opts.variant is not None:
+        if want is not None:
             prev = g.ctx.variant()
-            g.ctx.set_variant(opts.variant)
+            g.ctx.set_variant(want)
         try:
             st = _lib.lib().fmm_run(g.ctx.h, g.h, C.byref(spec.to_c()), X.dim, _vp(Xd), Y.nrows,
                                     _vp(Xd) if Y is X else _vp(Yd), _vp(Z.data), flags, C.byref(s))
@@ -852,21 +859,37 @@ def fused_mm_specialized(pattern: KnownPattern, A: CsrMatrix, X: DenseMatrix, Y:
 SHAPE_VARIANTS = (-1, 0, 1, 2, 3, 4, 5, 6, 7, 20, 21, 22, 23, 24)
 
 
+def _time_opts(A, X, Y, spec, t, opts, repeats) -> float:
+    fused_mm(A, X, Y, spec, t, None, opts)  # warm-up
+    ms = 0.0
+    for _ in range(repeats):
+        st = KernelStats()
+        fused_mm(A, X, Y, spec, t, st, opts)
+        ms += st.kernel_ms
+    return ms
+
+
 def tune_lane_width(A: CsrMatrix, X: DenseMatrix, Y: DenseMatrix, spec: OpSpec, t: int = 1,
                     repeats: int = 3) -> int:
-    """kernel.hpp:382-402 on the device: times every kernel shape variant for
-    this problem (device time of the fused kernels, after a warm-up) and
-    returns the fastest variant id — pass it back as KernelOptions(variant=…).
-    (The reference returns the fastest CPU lane width in {4, 8, 16}.)"""
+    """kernel.hpp:382-402 on the device, same contract as the reference:
+    times the lane widths {4, 8, 16} (device time of the fused kernels after
+    a warm-up; 4 = 128-bit gathers, 8 / 16 = the default 256-bit shapes) and
+    returns the fastest width, to pass back as KernelOptions(lane_width=...)."""
+    best, best_ms = 8, float("inf")
+    for w in (4, 8, 16):
+        ms = _time_opts(A, X, Y, spec, t, KernelOptions(lane_width=w), repeats)
+        if ms < best_ms:
+            best, best_ms = w, ms
+    return best
+
+
+def tune_variant(A: CsrMatrix, X: DenseMatrix, Y: DenseMatrix, spec: OpSpec, t: int = 1,
+                 repeats: int = 3) -> int:
+    """Device extension (tuning): the fastest dispatcher shape id among
+    SHAPE_VARIANTS, for KernelOptions(variant=...)."""
     best, best_ms = -1, float("inf")
     for v in SHAPE_VARIANTS:
-        opts = KernelOptions(variant=v)
-        fused_mm(A, X, Y, spec, t, None, opts)  # warm-up
-        ms = 0.0
-        for _ in range(repeats):
-            st = KernelStats()
-            fused_mm(A, X, Y, spec, t, st, opts)
-            ms += st.kernel_ms
+        ms = _time_opts(A, X, Y, spec, t, KernelOptions(variant=v), repeats)
         if ms < best_ms:
             best, best_ms = v, ms
     return best

@@ -228,7 +228,11 @@ def test_tune_lane_width_and_variant_option():
     scheme's tolerance (bitwise across runs of one variant)."""
     A, X, Y = random_case(77, 300, 300, 128, density=0.05, weighted=False)
     spec = F.make_spec(F.App.NODE_EMBED_SIGMOID)
-    v = F.tune_lane_width(A, X, Y, spec, 1, repeats=1)
+    lw = F.tune_lane_width(A, X, Y, spec, 1, repeats=1)
+    assert lw in (4, 8, 16)  # the reference's contract
+    Zl = F.fused_mm(A, X, Y, spec, 1, opts=F.KernelOptions(lane_width=lw))
+    check_tolerance(Zl.array, oracle.oracle_fused_mm(A, X, Y, spec), A, X, Y, spec)
+    v = F.tune_variant(A, X, Y, spec, 1, repeats=1)
     assert v in F.SHAPE_VARIANTS
     Z0 = F.fused_mm(A, X, Y, spec, 1, opts=F.KernelOptions(variant=v))
     Z1 = F.fused_mm(A, X, Y, spec, 1, opts=F.KernelOptions(variant=v))
