@@ -1,10 +1,15 @@
-"""Projected multi-GPU step time per config from measured pieces (no GPU):
-the slowest shard's kernel time at G shards (profiles/r06_shard_balance.jsonl,
-each shard run alone on one B200, cost-balanced part1d) and the largest
-per-GPU halo ingress (profiles/r2_halo_volume_c*.jsonl) over NVLink at the
-peer bandwidth a kernel's P2P traffic reaches (775 GB/s, measured on B300
-NV18, B300_MICROARCH.md). The exchange rides on the kernel's own stores, so
-a step is max(compute, ingress / bandwidth). A projection, not a measurement.
+"""Projected multi-GPU step time per config from measured pieces (no GPU).
+
+* compute: the slowest shard's kernel time at G shards WITH its halo stores
+  (profiles/r2v_shard_balance.jsonl, tools/shard_balance.py --halo: each
+  shard run alone on one B200, cost-balanced part1d, the stores going to
+  local stand-in peer buffers);
+* NVLink: the largest per-GPU halo ingress (profiles/r2_halo_volume_c*.jsonl)
+  and egress (the same r2v lines) at the peer bandwidth a kernel's P2P
+  traffic reaches (775 GB/s per direction, B300 NV18, B300_MICROARCH.md).
+
+The exchange rides on the kernel's own stores, so a step is
+max(compute, ingress / bw, egress / bw). A projection, not a measurement.
 
     python tools/scaling_projection.py > profiles/r2_scaling_projection.txt
 """
@@ -16,27 +21,33 @@ BW = 775e9
 
 
 def main():
-    bal = [json.loads(l) for l in (P / "r06_shard_balance.jsonl").read_text().splitlines() if l.strip()]
+    lines = [json.loads(l) for l in (P / "r2v_shard_balance.jsonl").read_text().splitlines() if l.strip()]
     halo = {}
     for f in sorted(P.glob("r2_halo_volume_c*.jsonl")):
         for l in f.read_text().splitlines():
             r = json.loads(l)
             halo[(r["config"], r["gpus"])] = r
-    print("config gpus compute_ms compute_x ingress_ms(halo) ingress_ms(all rows) projected_x(halo) projected_x(all rows)")
+    print("config gpus t1_ms compute_ms(+halo stores) ingress_ms egress_ms step_ms projected_x "
+          "| all-rows: ingress_ms projected_x")
     for c in (2, 3, 5):
-        pick = {b["gpus"]: b for b in bal if b["config"] == c and b["partition"] == "weighted"}
-        if 1 not in pick:
+        one = [r for r in lines if r["config"] == c and r["gpus"] == 1]
+        if not one:
             continue
-        t1 = pick[1]["max_ms"]
+        t1 = min(r["max_ms"] for r in one)
         for g in (2, 4, 8):
-            if g not in pick or (c, g) not in halo:
+            rs = [r for r in lines if r["config"] == c and r["gpus"] == g and r["halo_stores"]]
+            if not rs or (c, g) not in halo:
                 continue
-            comp = pick[g]["max_ms"]
-            h = halo[(c, g)]
-            ing = h["max_ingress_bytes"] / BW * 1e3
-            ing_all = h["max_ingress_bytes_all_rows"] / BW * 1e3
-            print(f"{c} {g} {comp:.3f} {t1 / comp:.2f} {ing:.3f} {ing_all:.3f} "
-                  f"{t1 / max(comp, ing):.2f} {t1 / max(comp, ing_all):.2f}")
+            r = rs[0]
+            comp = r["max_ms"]
+            ing = halo[(c, g)]["max_ingress_bytes"] / BW * 1e3
+            egr = max(r["halo_bytes_sent_per_shard"]) / BW * 1e3
+            step = max(comp, ing, egr)
+            ing_all = halo[(c, g)]["max_ingress_bytes_all_rows"] / BW * 1e3
+            egr_all = max(halo[(c, g)]["max_ingress_bytes_all_rows"], 0) / BW * 1e3  # all rows: egress ~ slice*(G-1)
+            step_all = max(comp, ing_all, egr_all)
+            print(f"{c} {g} {t1:.3f} {comp:.3f} {ing:.3f} {egr:.3f} {step:.3f} {t1 / step:.2f} "
+                  f"| {ing_all:.3f} {t1 / step_all:.2f}")
 
 
 if __name__ == "__main__":
