@@ -164,12 +164,13 @@ def cpu_sample(w, max_nnz: int = CPU_SAMPLE_NNZ):
                        f"Y = full X")
 
 
-def cpu_reference_run(w, steps: int, warmup: int, budget_s: float | None):
+def cpu_reference_run(w, steps: int, warmup: int, budget_s: float | None, threads: int | None = None):
     """Time the reference fused_mm<float> (oracle/_ref) or, when it was not
-    built, the C restatement (oracle port) on all host threads. Returns the
-    per-step seconds and the sample's nnz*d (the unit the rate counts)."""
+    built, the C restatement (oracle port) on all host threads (or
+    `threads`). Returns the per-step seconds and the sample's nnz*d (the unit
+    the rate counts)."""
     import oracle
-    threads = oracle.host_threads()
+    threads = threads or oracle.host_threads()
     As, Xs, Y, sample = cpu_sample(w)
     if oracle.ref_available():
         call = oracle.RefCall(As, Xs, Y, w.spec)
@@ -426,6 +427,9 @@ def run_ours(args):
         sec = sum(times) / len(times)
         cpu = {"value": nnzd_s / sec, "unit": "nnz*d/s", "cores": threads, "kind": kind,
                "sample": f"{sample} x{len(times)} (1 warm-up), all host threads"}
+        # the reference's single-thread rate beside it
+        _, _, t1, nnzd_1, _ = cpu_reference_run(w, 1, 0, budget_s=None, threads=1)
+        cpu["value_1_thread"] = nnzd_1 / t1[0]
 
     if world > 1 and iterative:
         sh.unmap_peer_buffers()
