@@ -91,8 +91,12 @@ def _approx_equal(a: np.ndarray, b: np.ndarray, rel_tol: float) -> bool:
 
 def run_bench(A: F.CsrMatrix, graph_name: str, spec: F.OpSpec, app_name: str, dims: Sequence[int],
               threads: Sequence[int], iterations: int, mode: BenchMode = BenchMode.BOTH,
-              seed: int = 42) -> list:
-    """bench.hpp:64-150 on the device: one record per (d, shard count)."""
+              seed: int = 42, opts: F.KernelOptions | None = None) -> list:
+    """bench.hpp:64-150 on the device: one record per (d, shard count).
+    opts: the fused call's options (e.g. KernelOptions(exact=False) to time
+    the reassociating scheme, which is what the unfused device pipeline
+    uses — the reference's own comparison is tolerance-based, bench.hpp:139)."""
+    fl = F._flags(opts)
     import torch
     from .configs import uniform_fill
 
@@ -110,11 +114,11 @@ def run_bench(A: F.CsrMatrix, graph_name: str, spec: F.OpSpec, app_name: str, di
                 with F.Context([i % max(F.device_count(), 1) for i in range(t)]) as ctx:
                     with F.DeviceGraph(ctx, A) as g:
                         Zf = np.zeros((A.nrows, d), np.float32)
-                        st = g.run_host(X, Y, Zf, d, spec)  # warm-up
+                        st = g.run_host(X, Y, Zf, d, spec, fl)  # warm-up
                         rec.fused_aux_bytes = int(st.aux_bytes)
                         ms = 0.0
                         for _ in range(iterations):
-                            ms += g.run_host(X, Y, Zf, d, spec).kernel_ms
+                            ms += g.run_host(X, Y, Zf, d, spec, fl).kernel_ms
                 rec.fused_seconds = ms / 1e3 / max(iterations, 1)
                 if rec.fused_seconds > 0:
                     rec.achieved_gflops = flop_count(gs.nnz, d) / rec.fused_seconds / 1e9
