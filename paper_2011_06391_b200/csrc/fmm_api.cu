@@ -364,6 +364,22 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
         p.n_narrow_rows = rows;
     }
     if (p.n_chunk_items + p.n_wide_rows + p.n_narrow_rows == 0) return 0;
+    if (d <= fmm::kMaxRegDim) {
+        // empty rows sort last: they leave the narrow list and only get the
+        // AOP identity, from the wide warps' prologues (up to kZeroPerWideMax
+        // rows each) and from dedicated warps for the remainder
+        static const bool zero_narrow = std::getenv("FMM_ZERO_NARROW") != nullptr;  // tuning: the old path
+        if (!zero_narrow) {
+            p.n_zero_rows = rows - gs.nonempty;
+            p.n_narrow_rows -= p.n_zero_rows;
+            const int64_t wide_warps = p.n_chunk_items + p.n_wide_rows;
+            if (wide_warps > 0 && p.n_zero_rows > 0) {
+                const int64_t per = std::min<int64_t>((p.n_zero_rows + wide_warps - 1) / wide_warps, fmm::kZeroPerWideMax);
+                p.zero_per_wide = static_cast<int>(per);
+                p.n_zero_piggy = std::min<int64_t>(p.n_zero_rows, per * wide_warps);
+            }
+        }
+    }
     if (d > fmm::kMaxRegDim) {
         // any d past the register-resident shapes: the streamed kernel tiles
         // d (reference: the d > 256 second sweep, kernel.hpp:192-225); rows

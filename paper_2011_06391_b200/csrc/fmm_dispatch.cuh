@@ -3,6 +3,8 @@
 // instantiations compile in parallel.
 #pragma once
 
+#include <type_traits>
+
 #include "fmm_kernels.cuh"
 
 namespace fmm {
@@ -12,22 +14,36 @@ namespace fmm {
 // load it now rather than inside the caller's first fused_mm call.
 inline thread_local bool t_preload = false;
 
-template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED, int MINB = 0, int PF = -1>
+template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED, int MINB = 0, int PF = -1, int OPT = 0>
 inline void launch_one(const KParams& p, const Ops& ops, cudaStream_t stream) {
     if (t_preload) {
         cudaFuncAttributes a;
-        cudaFuncGetAttributes(&a, fmm_rows_kernel<Ops, LPG, VEC, NV, UNROLL, EXACT, MASKED, MINB, PF>);
+        cudaFuncGetAttributes(&a, fmm_rows_kernel<Ops, LPG, VEC, NV, UNROLL, EXACT, MASKED, MINB, PF, OPT>);
         return;
     }
     constexpr int kThreads = 256;
     constexpr int GPW = 32 / LPG;
     const int64_t wide = EXACT ? 0 : p.n_chunk_items + p.n_wide_rows;
-    const int64_t warps = wide + (p.n_narrow_rows + GPW - 1) / GPW;
+    const int64_t zero_left = p.n_zero_rows - p.n_zero_piggy;
+    const int64_t warps = wide + (p.n_narrow_rows + GPW - 1) / GPW + (zero_left + kZeroRowsPerWarp - 1) / kZeroRowsPerWarp;
     if (warps <= 0) return;
     const int64_t blocks = (warps + (kThreads / 32) - 1) / (kThreads / 32);
-    fmm_rows_kernel<Ops, LPG, VEC, NV, UNROLL, EXACT, MASKED, MINB, PF>
+    fmm_rows_kernel<Ops, LPG, VEC, NV, UNROLL, EXACT, MASKED, MINB, PF, OPT>
         <<<static_cast<unsigned>(blocks), kThreads, 0, stream>>>(p, ops);
 }
+
+#ifdef FMM_TUNING_VARIANTS
+// variants 40 + OPT (OPT = 1..15): the default shape with row-kernel option bits
+template <class Ops, int LPG, int VEC, int NV, int U, int MINB, int PF, int O = 1>
+inline bool launch_opt(const KParams& p, const Ops& ops, int opt, cudaStream_t s) {
+    if constexpr (O > 15 || !(std::is_same_v<Ops, OpsSigmoid> || std::is_same_v<Ops, OpsTdist>)) {
+        return false;
+    } else {
+        if (opt == O) { launch_one<Ops, LPG, VEC, NV, U, false, false, MINB, PF, O>(p, ops, s); return true; }
+        return launch_opt<Ops, LPG, VEC, NV, U, MINB, PF, O + 1>(p, ops, opt, s);
+    }
+}
+#endif
 
 // Vectorised shapes: d = LPG * VEC * NV exactly, rows VEC*4-byte aligned.
 // variant < 0 selects the default shape for d. The shipped library holds the
@@ -48,6 +64,18 @@ inline bool launch_aligned32(const KParams& p, const Ops& ops, int d, int varian
                 if (variant == 21) { launch_one<Ops, 2, 8, 2, 4, EXACT, false, 3, 1>(p, ops, s); return true; }
                 if (variant == 22) { launch_one<Ops, 4, 8, 1, 8, EXACT, false, 3, 1>(p, ops, s); return true; }
                 if (variant == 23) { launch_one<Ops, 4, 8, 1, 4, EXACT, false, 4, 1>(p, ops, s); return true; }
+                if (variant == 24) { launch_one<Ops, 4, 8, 1, 2, EXACT, false, 4, 1>(p, ops, s); return true; }
+                if (variant == 25) { launch_one<Ops, 4, 8, 1, 2, EXACT, false, 5, 1>(p, ops, s); return true; }
+                if (variant == 26) { launch_one<Ops, 4, 8, 1, 4, EXACT, false, 3, 1>(p, ops, s); return true; }
+                if (variant == 27) { launch_one<Ops, 4, 4, 2, 2, EXACT, false, 5, 1>(p, ops, s); return true; }
+                if (variant == 28) { launch_one<Ops, 4, 8, 1, 2, EXACT, false, 6, 1>(p, ops, s); return true; }
+                if (variant == 29) { launch_one<Ops, 8, 4, 1, 2, EXACT, false, 6, 1>(p, ops, s); return true; }
+                if (variant == 30) { launch_one<Ops, 8, 4, 1, 4, EXACT, false, 5, 1>(p, ops, s); return true; }
+                if (variant >= 40 && launch_opt<Ops, 4, 4, 2, 2, 4, 1>(p, ops, variant - 40, s)) return true;
+                if (variant == 56) { launch_one<Ops, 4, 4, 2, 2, EXACT, false, 3, 1, 16>(p, ops, s); return true; }
+                if (variant == 57) { launch_one<Ops, 4, 4, 2, 1, EXACT, false, 4, 1, 16>(p, ops, s); return true; }
+                if (variant == 58) { launch_one<Ops, 4, 8, 1, 2, EXACT, false, 3, 1, 16>(p, ops, s); return true; }
+                if (variant == 59) { launch_one<Ops, 4, 8, 1, 1, EXACT, false, 4, 1, 16>(p, ops, s); return true; }
             }
 #endif
             // config 3 keeps the VEC = 4 shape (0.616 ms; VEC = 8 U = 2: 0.618)
@@ -61,6 +89,11 @@ inline bool launch_aligned32(const KParams& p, const Ops& ops, int d, int varian
                 if (variant == 22) { launch_one<Ops, 16, 8, 1, 4, EXACT, false>(p, ops, s); return true; }
                 if (variant == 23) { launch_one<Ops, 8, 8, 2, 2, EXACT, false>(p, ops, s); return true; }
                 if (variant == 24) { launch_one<Ops, 8, 8, 2, 4, EXACT, false, 3>(p, ops, s); return true; }
+                if (variant >= 40 && launch_opt<Ops, 8, 8, 2, 4, 2, -1>(p, ops, variant - 40, s)) return true;
+                if (variant == 56) { launch_one<Ops, 8, 8, 2, 2, EXACT, false, 2, -1, 16>(p, ops, s); return true; }
+                if (variant == 57) { launch_one<Ops, 8, 8, 2, 2, EXACT, false, 0, -1, 16>(p, ops, s); return true; }
+                if (variant == 58) { launch_one<Ops, 8, 8, 2, 1, EXACT, false, 3, -1, 16>(p, ops, s); return true; }
+                if (variant == 59) { launch_one<Ops, 8, 8, 2, 4, EXACT, false, 0, -1, 16>(p, ops, s); return true; }
 #endif
                 launch_one<Ops, 8, 8, 2, 4, EXACT, false>(p, ops, s); return true;  // config 2
             }
@@ -71,6 +104,9 @@ inline bool launch_aligned32(const KParams& p, const Ops& ops, int d, int varian
                 if (variant == 21) { launch_one<Ops, 16, 8, 2, 4, EXACT, false>(p, ops, s); return true; }
                 if (variant == 22) { launch_one<Ops, 8, 8, 4, 2, EXACT, false>(p, ops, s); return true; }
                 if (variant == 25) { launch_one<Ops, 32, 8, 1, 8, EXACT, false>(p, ops, s); return true; }
+                if (variant >= 40 && launch_opt<Ops, 32, 8, 1, 4, 0, -1>(p, ops, variant - 40, s)) return true;
+                if (variant == 56) { launch_one<Ops, 32, 8, 1, 2, EXACT, false, 3, -1, 16>(p, ops, s); return true; }
+                if (variant == 57) { launch_one<Ops, 32, 8, 1, 4, EXACT, false, 2, -1, 16>(p, ops, s); return true; }
 #endif
                 // config 5: a warp per row-group of 32 lanes x 32 B (80 registers)
                 launch_one<Ops, 32, 8, 1, 4, EXACT, false>(p, ops, s); return true;

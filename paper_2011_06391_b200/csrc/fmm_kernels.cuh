@@ -35,6 +35,16 @@ constexpr int kMaxPeers = 7;  // 8 GPUs per NVSwitch domain in one process
 // Largest d the register-resident row kernels hold (masked shapes: 32 lanes
 // x 32 values); beyond it the streamed kernel (fmm_k_stream.cu) tiles d.
 constexpr int kMaxRegDim = 1024;
+// empty rows one dedicated warp (or, at most, one wide warp) fills
+constexpr int kZeroRowsPerWarp = 64;
+constexpr int kZeroPerWideMax = 32;
+
+// Row-kernel option bits (template parameter OPT)
+constexpr int kOptFast = 1;    // full sub-batches run an unpredicated copy of the loop body
+constexpr int kOptDotIlv = 2;  // the U dot products advance interleaved
+constexpr int kOptPfL2 = 4;    // neighbour rows of the next column batch prefetched into L2
+constexpr int kOptPfL1 = 8;    // neighbour rows of the next sub-batch prefetched into L1
+constexpr int kOptPipe = 16;   // wide rows: two half-size sub-batches alternate, one in flight while the other is consumed
 
 struct PeerOut {
     float* p[kMaxPeers];
@@ -66,7 +76,15 @@ struct KParams {
     int fold_max;            // AOP is AMAX
     int64_t n_chunk_items;
     int64_t n_wide_rows;     // rows a whole warp folds (edges over its groups)
-    int64_t n_narrow_rows;   // rows one lane group folds
+    int64_t n_narrow_rows;   // rows one lane group folds (non-empty ones)
+    // empty rows (order slots after the narrow rows) only receive the AOP
+    // identity: wide warp w writes slots [w*zero_per_wide, (w+1)*zero_per_wide)
+    // of the first n_zero_piggy while it waits for its own x_u / column
+    // loads; the rest go to dedicated warps at the end of the grid, each
+    // writing kZeroRowsPerWarp rows
+    int64_t n_zero_rows;
+    int64_t n_zero_piggy;
+    int zero_per_wide;
     int64_t row0;
     int chunk;               // edges per chunk (fast scheme)
     int d;
@@ -279,6 +297,15 @@ __device__ __forceinline__ float ld_stream_f32(const float* p) {
     return v;
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+// one prefetch per 128-byte line of a d-float row
+template <int D>
+__device__ __forceinline__ void prefetch_row_l2(const float* row) {
+#pragma unroll
+    for (int b = 0; b < D * 4; b += 128) prefetch_l2(reinterpret_cast<const char*>(row) + b);
+}
+
 // xor-butterfly over the LPR lanes of a group; every lane ends with the same
 // bits (a+b == b+a in IEEE arithmetic), so all lanes agree on h.
 template <int LPR>
@@ -335,7 +362,7 @@ __device__ __forceinline__ constexpr int transposed_lane(int u) {
 // --------------------------------------------------------------- the kernel
 // Per-edge work for U gathered neighbour rows: ROP across the group, SOP,
 // MOP, AOP into z (update_u's loop body, kernel.hpp:92-106).
-template <class Ops, int LPG, int VEC, int NV, int U, bool EXACT, bool MASKED>
+template <class Ops, int LPG, int VEC, int NV, int U, bool EXACT, bool MASKED, int OPT = 0>
 __device__ __forceinline__ void consume_edges(const Ops& ops, const KParams& p, const float (&x)[NV * VEC],
                                               float (&z)[NV * VEC], const float (&y)[U][NV * VEC],
                                               const float (&a)[U], const bool (&ok)[U],
@@ -351,6 +378,37 @@ __device__ __forceinline__ void consume_edges(const Ops& ops, const KParams& p, 
         if (!EXACT && ops.aop() == FMM_AOP_ASUM && ops.rop() != FMM_ROP_NOOP &&
             ops.rop() != FMM_ROP_RMUL && ops.mop() != FMM_MOP_SEL2ND && ops.vop() != FMM_VOP_MLP) {
             float s[U];
+            if constexpr ((OPT & kOptDotIlv) != 0) {
+                // the U x 2 accumulator chains advance together (element pair
+                // outer, edge inner): consecutive FFMA2 are independent
+                float2 acc[U][2];
+#pragma unroll
+                for (int u = 0; u < U; ++u) acc[u][0] = acc[u][1] = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int e = 0; e < NE; e += 2) {
+                    const float2 xv = make_float2(x[e], x[e + 1]);
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const float2 yv = make_float2(y[u][e], y[u][e + 1]);
+                        float2& a2 = acc[u][(e >> 1) & 1];
+                        if (ops.vop() == FMM_VOP_MUL && ops.rop() == FMM_ROP_RSUM) {
+                            a2 = __ffma2_rn(xv, yv, a2);
+                        } else {
+                            float2 t;
+                            switch (ops.vop()) {
+                                case FMM_VOP_ADD: t = __fadd2_rn(xv, yv); break;
+                                case FMM_VOP_MUL: t = __fmul2_rn(xv, yv); break;
+                                case FMM_VOP_SEL2ND: t = yv; break;
+                                default: t = __ffma2_rn(yv, make_float2(-1.f, -1.f), xv); break;  // x - y
+                            }
+                            if (ops.rop() == FMM_ROP_RSUM) a2 = __fadd2_rn(a2, t);
+                            else a2 = __ffma2_rn(t, t, a2);  // NORM / SQNORM
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) s[u] = (acc[u][0].x + acc[u][0].y) + (acc[u][1].x + acc[u][1].y);
+            } else
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
@@ -505,7 +563,7 @@ __device__ __forceinline__ void consume_edges(const Ops& ops, const KParams& p, 
     }
 }
 
-template <int LPG, int VEC, int NV, int U, bool MASKED>
+template <int LPG, int VEC, int NV, int U, bool MASKED, bool ALLOK = false>
 __device__ __forceinline__ void gather_rows(const float* __restrict__ Y, int d, const int (&v)[U],
                                             const bool (&ok)[U], const bool (&elem_ok)[NV], int gl,
                                             float (&y)[U][NV * VEC]) {
@@ -514,7 +572,7 @@ __device__ __forceinline__ void gather_rows(const float* __restrict__ Y, int d, 
         const float* yr = Y + static_cast<int64_t>(v[u]) * d;
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
-            if (ok[u] && elem_ok[i]) {
+            if ((ALLOK || ok[u]) && elem_ok[i]) {
                 load_vec<VEC>(&y[u][i * VEC], yr + (i * LPG + gl) * VEC);
             } else {
 #pragma unroll
@@ -534,7 +592,7 @@ __device__ __forceinline__ void gather_rows(const float* __restrict__ Y, int d, 
 // Lane layout: element j = (i*LPG + lane_in_group)*VEC + c.
 // MINB = 0 leaves the register budget to ptxas (as __launch_bounds__(256));
 // MINB > 0 asks for that many resident blocks per SM (tuning variants).
-template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED, int MINB = 0, int PF = -1>
+template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED, int MINB = 0, int PF = -1, int OPT = 0>
 __global__ void __launch_bounds__(256, MINB)
 fmm_rows_kernel(const KParams p, const Ops ops) {
     constexpr int NE = NV * VEC;
@@ -546,6 +604,10 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
     // registers cost more than the hidden index latency (measured).
     // PF: -1 = this rule, 0 / 1 = forced (tuning variants)
     constexpr bool kPrefetchCols = PF >= 0 ? (PF == 1) : (!EXACT && !MASKED && (LPG * VEC * NV >= 128));
+    constexpr bool kFast = (OPT & kOptFast) != 0 && !EXACT && !MASKED;
+    constexpr bool kPfL2 = (OPT & kOptPfL2) != 0 && kPrefetchCols && !MASKED;
+    constexpr bool kPfL1 = (OPT & kOptPfL1) != 0 && kPrefetchCols && !MASKED;
+    constexpr bool kPipe = (OPT & kOptPipe) != 0 && kPrefetchCols && !MASKED && !EXACT;
 
     const int lane = threadIdx.x & 31;
     const int gl = lane & (LPG - 1);
@@ -558,6 +620,7 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
     int64_t r = 0, e0 = 0, e1 = 0;
     float* out = nullptr;
     bool active;
+    int64_t zero_warp = -1;
     if (wide) {
         active = true;
         if (warp < p.n_chunk_items) {
@@ -576,7 +639,8 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
     } else {
         const int64_t idx = (warp - n_wide_items) * GPW + g;
         active = idx < p.n_narrow_rows;
-        if (__all_sync(0xffffffffu, !active)) return;
+        zero_warp = warp - n_wide_items - (p.n_narrow_rows + GPW - 1) / GPW;  // >= 0: a dedicated empty-row warp
+        if (zero_warp < 0 && __all_sync(0xffffffffu, !active)) return;
         if (active) {
             const int4 it = __ldg(p.items + (p.n_wide_rows + idx));
             r = it.x;
@@ -605,6 +669,42 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
             if (elem_ok[i]) load_vec<VEC>(&x[i * VEC], xr + (i * LPG + gl) * VEC);
     }
 
+    // AOP identity into the empty rows of order slots [zs, zs + zn) (relative
+    // to the first empty slot): lane l fetches row id zs + l, the lane groups
+    // then store GPW rows per step. Returns with nothing pending but stores.
+    auto fill_empty_rows = [&](int64_t zs, int zn) {
+        const int32_t* zorder = p.order + p.n_wide_rows + p.n_narrow_rows + zs;
+        float idv[VEC];
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) idv[c] = ident;
+        for (int b0 = 0; b0 < zn; b0 += 32) {
+            const int rid = (b0 + lane < zn) ? __ldg(zorder + b0 + lane) : 0;
+            const int lim = min(32, zn - b0);  // warp-uniform
+            for (int j = 0; j < lim; j += GPW) {
+                const int zr = __shfl_sync(0xffffffffu, rid, j + g);
+                if (j + g < lim) {
+                    const unsigned zpm = p.n_peer > 0 ? peer_bits(p.peer_mask, zr) : 0u;
+                    float* zo = p.Z + static_cast<int64_t>(zr) * d;
+#pragma unroll
+                    for (int i = 0; i < NV; ++i)
+                        if (elem_ok[i]) {
+                            store_vec<VEC>(zo + (i * LPG + gl) * VEC, idv);
+                            for (int q = 0; q < p.n_peer; ++q)
+                                if ((zpm >> q) & 1u)
+                                    store_vec<VEC>(p.zpeer[q] + static_cast<int64_t>(zr) * d + (i * LPG + gl) * VEC, idv);
+                        }
+                }
+            }
+        }
+    };
+
+    if (zero_warp >= 0) {
+        const int64_t zs = p.n_zero_piggy + zero_warp * kZeroRowsPerWarp;
+        if (zs < p.n_zero_rows)
+            fill_empty_rows(zs, static_cast<int>(min(static_cast<int64_t>(kZeroRowsPerWarp), p.n_zero_rows - zs)));
+        return;
+    }
+
     if (wide) {
         // ---- one item per warp; edge k of the item goes to group k % GPW
         constexpr int SB = GPW * U;                   // edges per sub-batch
@@ -627,6 +727,60 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
             }
         };
         if constexpr (kPrefetchCols) fetch(0);
+        // this warp's share of the empty rows, written while x_u and the first
+        // column batch are on their way
+        if (p.zero_per_wide > 0) {
+            const int64_t zs = warp * p.zero_per_wide;
+            if (zs < p.n_zero_piggy)
+                fill_empty_rows(zs, static_cast<int>(min(static_cast<int64_t>(p.zero_per_wide), p.n_zero_piggy - zs)));
+        }
+        if constexpr (kPipe && KPL == 1) {
+            // software pipeline over sub-batches t = 0 .. T-1 of SB edges: the
+            // gathers of t+1 are issued before t is consumed, into the other
+            // of two register buffers (same registers as one sub-batch of 2U)
+            int cidx = cnext[0];
+            float aval = anext[0];
+            int ib = 0;  // first edge of the column batch held in cidx
+            if (B < n) fetch(B);
+            const int T = (n + SB - 1) / SB;
+            auto issue = [&](int t, float (&y)[U][NE], float (&a)[U]) {
+                const int e = t * SB;
+                if (e >= ib + B) {
+                    cidx = cnext[0];
+                    aval = anext[0];
+                    ib += B;
+                    if (ib + B < n) fetch(ib + B);
+                }
+                const int s = e - ib;
+                int v[U];
+                bool ok[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int src = ((s + u * GPW) % 32) + g;
+                    v[u] = __shfl_sync(0xffffffffu, cidx, src);
+                    a[u] = has_val ? __shfl_sync(0xffffffffu, aval, src) : 1.0f;
+                    ok[u] = (e + u * GPW + g) < n;
+                }
+                gather_rows<LPG, VEC, NV, U, MASKED>(p.Y, d, v, ok, elem_ok, gl, y);
+            };
+            auto consume = [&](int t, const float (&y)[U][NE], const float (&a)[U]) {
+                bool ok[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) ok[u] = (t * SB + u * GPW + g) < n;
+                consume_edges<Ops, LPG, VEC, NV, U, EXACT, MASKED, OPT>(ops, p, x, z, y, a, ok, elem_ok);
+            };
+            float ya[U][NE], yb[U][NE], aa[U], ab[U];
+            if (T > 0) issue(0, ya, aa);
+#pragma unroll 1
+            for (int t = 0; t < T; t += 2) {
+                if (t + 1 < T) issue(t + 1, yb, ab);
+                consume(t, ya, aa);
+                if (t + 1 < T) {
+                    if (t + 2 < T) issue(t + 2, ya, aa);
+                    consume(t + 1, yb, ab);
+                }
+            }
+        } else
         for (int base = 0; base < n; base += B) {
             if constexpr (!kPrefetchCols) fetch(base);
             int cidx[KPL];
@@ -657,8 +811,42 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
                     ok[u] = (base + bq + g) < n;
                 }
                 float y[U][NE];
-                gather_rows<LPG, VEC, NV, U, MASKED>(p.Y, d, v, ok, elem_ok, gl, y);
-                consume_edges<Ops, LPG, VEC, NV, U, EXACT, MASKED>(ops, p, x, z, y, a, ok, elem_ok);
+                const bool full = kFast && (base + s + SB <= n);  // warp-uniform
+                if (full) gather_rows<LPG, VEC, NV, U, MASKED, true>(p.Y, d, v, ok, elem_ok, gl, y);
+                else gather_rows<LPG, VEC, NV, U, MASKED>(p.Y, d, v, ok, elem_ok, gl, y);
+                if constexpr (kPfL2) {
+                    // the next column batch has arrived by now: its rows start
+                    // towards L2 a sub-batch (or more) before they are gathered
+                    if (s == 0 && base + B < n) {
+#pragma unroll
+                        for (int q = 0; q < KPL; ++q)
+                            if (base + B + q * 32 + lane < n)
+                                prefetch_row_l2<LPG * VEC * NV>(p.Y + static_cast<int64_t>(cnext[q]) * d);
+                    }
+                }
+                if constexpr (kPfL1 && KPL == 1) {
+                    // rows of the following sub-batch into L1
+                    const int sn = s + SB;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int bq = sn + u * GPW;
+                        const int c = bq < B ? __shfl_sync(0xffffffffu, cidx[0], (bq % 32) + g)
+                                             : __shfl_sync(0xffffffffu, cnext[0], ((bq - B) % 32) + g);
+                        if (base + bq + g < n) {
+                            const float* yr = p.Y + static_cast<int64_t>(c) * d;
+#pragma unroll
+                            for (int i = 0; i < NV; ++i) prefetch_l1(yr + (i * LPG + gl) * VEC);
+                        }
+                    }
+                }
+                if (full) {
+                    bool okt[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) okt[u] = true;
+                    consume_edges<Ops, LPG, VEC, NV, U, EXACT, MASKED, OPT>(ops, p, x, z, y, a, okt, elem_ok);
+                } else {
+                    consume_edges<Ops, LPG, VEC, NV, U, EXACT, MASKED, OPT>(ops, p, x, z, y, a, ok, elem_ok);
+                }
             }
         }
         // fold the GPW group partials (fixed butterfly order -> deterministic)
@@ -801,8 +989,38 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
                     ok[u] = (base + b) < n;
                 }
                 float y[U][NE];
-                gather_rows<LPG, VEC, NV, U, MASKED>(p.Y, d, v, ok, elem_ok, gl, y);
-                consume_edges<Ops, LPG, VEC, NV, U, EXACT, MASKED>(ops, p, x, z, y, a, ok, elem_ok);
+                const bool full = kFast && __all_sync(0xffffffffu, base + u0 + U <= n);
+                if (full) gather_rows<LPG, VEC, NV, U, MASKED, true>(p.Y, d, v, ok, elem_ok, gl, y);
+                else gather_rows<LPG, VEC, NV, U, MASKED>(p.Y, d, v, ok, elem_ok, gl, y);
+                if constexpr (kPfL2) {
+                    if (u0 == 0 && base + B < nmax) {
+#pragma unroll
+                        for (int q = 0; q < KPL; ++q)
+                            if (base + B + q * LPG + gl < n)
+                                prefetch_row_l2<LPG * VEC * NV>(p.Y + static_cast<int64_t>(cnext[q]) * d);
+                    }
+                }
+                if constexpr (kPfL1 && KPL == 1) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int b = u0 + U + u;
+                        const int c = b < B ? __shfl_sync(0xffffffffu, cidx[0], gbase + (b % LPG))
+                                            : __shfl_sync(0xffffffffu, cnext[0], gbase + ((b - B) % LPG));
+                        if (base + b < n) {
+                            const float* yr = p.Y + static_cast<int64_t>(c) * d;
+#pragma unroll
+                            for (int i = 0; i < NV; ++i) prefetch_l1(yr + (i * LPG + gl) * VEC);
+                        }
+                    }
+                }
+                if (full) {
+                    bool okt[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) okt[u] = true;
+                    consume_edges<Ops, LPG, VEC, NV, U, EXACT, MASKED, OPT>(ops, p, x, z, y, a, okt, elem_ok);
+                } else {
+                    consume_edges<Ops, LPG, VEC, NV, U, EXACT, MASKED, OPT>(ops, p, x, z, y, a, ok, elem_ok);
+                }
             }
         }
         if (active) {
