@@ -3,6 +3,7 @@
 // instantiations compile in parallel.
 #pragma once
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "fmm_kernels.cuh"
@@ -21,7 +22,28 @@ inline void launch_one(const KParams& p, const Ops& ops, cudaStream_t stream) {
         cudaFuncGetAttributes(&a, fmm_rows_kernel<Ops, LPG, VEC, NV, UNROLL, EXACT, MASKED, MINB, PF, OPT>);
         return;
     }
-    constexpr int kThreads = 256;
+    // Warps never cooperate across a block (no shared memory, no barrier), so
+    // the block is as small as the kernel's register-limited occupancy allows:
+    // a block's slot frees when its slowest warp is done, and with 8 warps per
+    // block that idled ~7% of the resident warps (r3: config 2 1.177 -> 1.136
+    // ms, config 3 0.456 -> 0.436 ms with one warp per block). 32 blocks per SM
+    // is the hardware limit, so kernels that fit more than 32 warps keep
+    // larger blocks. FMM_BLOCK_THREADS overrides (tuning).
+    static const int kThreads = [] {
+        if (const char* e = std::getenv("FMM_BLOCK_THREADS")) {
+            const int t = std::atoi(e);
+            if (t >= 32 && t <= 256 && t % 32 == 0) return t;
+        }
+        auto kern = fmm_rows_kernel<Ops, LPG, VEC, NV, UNROLL, EXACT, MASKED, MINB, PF, OPT>;
+        int full = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&full, kern, 256, 0) != cudaSuccess || full <= 0) return 256;
+        for (int t = 32; t < 256; t *= 2) {
+            int nb = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, t, 0) == cudaSuccess && nb * t >= full * 256)
+                return t;
+        }
+        return 256;
+    }();
     constexpr int GPW = 32 / LPG;
     const int64_t wide = EXACT ? 0 : p.n_chunk_items + p.n_wide_rows;
     const int64_t zero_left = p.n_zero_rows - p.n_zero_piggy;

@@ -582,6 +582,42 @@ __device__ __forceinline__ void gather_rows(const float* __restrict__ Y, int d, 
     }
 }
 
+// AOP identity into the empty rows at order slots [zs, zs + zn) (relative to
+// the first empty slot, which follows the narrow rows): lane l fetches row id
+// zs + l, the lane groups then store GPW rows per step, to Z and to every
+// peer that reads the row.
+template <class Ops, int LPG, int VEC, int NV, bool MASKED>
+__device__ __forceinline__ void fill_identity_rows(const KParams& p, const Ops& ops, int64_t zs, int zn) {
+    constexpr int GPW = 32 / LPG;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & (LPG - 1);
+    const int g = lane / LPG;
+    const int d = MASKED ? p.d : LPG * VEC * NV;
+    const int32_t* zorder = p.order + p.n_wide_rows + p.n_narrow_rows + zs;
+    float idv[VEC];
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) idv[c] = aop_identity(ops);
+    for (int b0 = 0; b0 < zn; b0 += 32) {
+        const int rid = (b0 + lane < zn) ? __ldg(zorder + b0 + lane) : 0;
+        const int lim = min(32, zn - b0);  // warp-uniform
+        for (int j = 0; j < lim; j += GPW) {
+            const int zr = __shfl_sync(0xffffffffu, rid, j + g);
+            if (j + g < lim) {
+                const unsigned zpm = p.n_peer > 0 ? peer_bits(p.peer_mask, zr) : 0u;
+                float* zo = p.Z + static_cast<int64_t>(zr) * d;
+#pragma unroll
+                for (int i = 0; i < NV; ++i)
+                    if (!MASKED || (i * LPG + gl) * VEC < d) {
+                        store_vec<VEC>(zo + (i * LPG + gl) * VEC, idv);
+                        for (int q = 0; q < p.n_peer; ++q)
+                            if ((zpm >> q) & 1u)
+                                store_vec<VEC>(p.zpeer[q] + static_cast<int64_t>(zr) * d + (i * LPG + gl) * VEC, idv);
+                    }
+            }
+        }
+    }
+}
+
 // Work items, in launch order (heaviest first, LPT-like):
 //   [0, n_chunk_items)                 chunk of a split row  -> wide warp
 //   [.., + n_wide_rows)                row order[i]          -> wide warp
@@ -616,11 +652,21 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
     const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t n_wide_items = EXACT ? 0 : p.n_chunk_items + p.n_wide_rows;
     const bool wide = warp < n_wide_items;  // warp-uniform
+    {
+        // warps past the narrow rows only write the AOP identity to empty rows
+        const int64_t zw = warp - n_wide_items - (p.n_narrow_rows + GPW - 1) / GPW;
+        if (zw >= 0) {
+            const int64_t zs = p.n_zero_piggy + zw * kZeroRowsPerWarp;
+            if (zs < p.n_zero_rows)
+                fill_identity_rows<Ops, LPG, VEC, NV, MASKED>(
+                    p, ops, zs, static_cast<int>(min(static_cast<int64_t>(kZeroRowsPerWarp), p.n_zero_rows - zs)));
+            return;
+        }
+    }
 
     int64_t r = 0, e0 = 0, e1 = 0;
     float* out = nullptr;
     bool active;
-    int64_t zero_warp = -1;
     if (wide) {
         active = true;
         if (warp < p.n_chunk_items) {
@@ -639,8 +685,7 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
     } else {
         const int64_t idx = (warp - n_wide_items) * GPW + g;
         active = idx < p.n_narrow_rows;
-        zero_warp = warp - n_wide_items - (p.n_narrow_rows + GPW - 1) / GPW;  // >= 0: a dedicated empty-row warp
-        if (zero_warp < 0 && __all_sync(0xffffffffu, !active)) return;
+        if (__all_sync(0xffffffffu, !active)) return;
         if (active) {
             const int4 it = __ldg(p.items + (p.n_wide_rows + idx));
             r = it.x;
@@ -667,42 +712,6 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
 #pragma unroll
         for (int i = 0; i < NV; ++i)
             if (elem_ok[i]) load_vec<VEC>(&x[i * VEC], xr + (i * LPG + gl) * VEC);
-    }
-
-    // AOP identity into the empty rows of order slots [zs, zs + zn) (relative
-    // to the first empty slot): lane l fetches row id zs + l, the lane groups
-    // then store GPW rows per step. Returns with nothing pending but stores.
-    auto fill_empty_rows = [&](int64_t zs, int zn) {
-        const int32_t* zorder = p.order + p.n_wide_rows + p.n_narrow_rows + zs;
-        float idv[VEC];
-#pragma unroll
-        for (int c = 0; c < VEC; ++c) idv[c] = ident;
-        for (int b0 = 0; b0 < zn; b0 += 32) {
-            const int rid = (b0 + lane < zn) ? __ldg(zorder + b0 + lane) : 0;
-            const int lim = min(32, zn - b0);  // warp-uniform
-            for (int j = 0; j < lim; j += GPW) {
-                const int zr = __shfl_sync(0xffffffffu, rid, j + g);
-                if (j + g < lim) {
-                    const unsigned zpm = p.n_peer > 0 ? peer_bits(p.peer_mask, zr) : 0u;
-                    float* zo = p.Z + static_cast<int64_t>(zr) * d;
-#pragma unroll
-                    for (int i = 0; i < NV; ++i)
-                        if (elem_ok[i]) {
-                            store_vec<VEC>(zo + (i * LPG + gl) * VEC, idv);
-                            for (int q = 0; q < p.n_peer; ++q)
-                                if ((zpm >> q) & 1u)
-                                    store_vec<VEC>(p.zpeer[q] + static_cast<int64_t>(zr) * d + (i * LPG + gl) * VEC, idv);
-                        }
-                }
-            }
-        }
-    };
-
-    if (zero_warp >= 0) {
-        const int64_t zs = p.n_zero_piggy + zero_warp * kZeroRowsPerWarp;
-        if (zs < p.n_zero_rows)
-            fill_empty_rows(zs, static_cast<int>(min(static_cast<int64_t>(kZeroRowsPerWarp), p.n_zero_rows - zs)));
-        return;
     }
 
     if (wide) {
@@ -732,7 +741,8 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
         if (p.zero_per_wide > 0) {
             const int64_t zs = warp * p.zero_per_wide;
             if (zs < p.n_zero_piggy)
-                fill_empty_rows(zs, static_cast<int>(min(static_cast<int64_t>(p.zero_per_wide), p.n_zero_piggy - zs)));
+                fill_identity_rows<Ops, LPG, VEC, NV, MASKED>(
+                    p, ops, zs, static_cast<int>(min(static_cast<int64_t>(p.zero_per_wide), p.n_zero_piggy - zs)));
         }
         if constexpr (kPipe && KPL == 1) {
             // software pipeline over sub-batches t = 0 .. T-1 of SB edges: the
