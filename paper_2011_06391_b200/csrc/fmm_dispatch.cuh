@@ -15,11 +15,11 @@ namespace fmm {
 // load it now rather than inside the caller's first fused_mm call.
 inline thread_local bool t_preload = false;
 
-template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED, int MINB = 0, int PF = -1, int OPT = 0>
+template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED, int MINB = 0, int PF = -1, int BT = 256>
 inline void launch_one(const KParams& p, const Ops& ops, cudaStream_t stream) {
     if (t_preload) {
         cudaFuncAttributes a;
-        cudaFuncGetAttributes(&a, fmm_rows_kernel<Ops, LPG, VEC, NV, UNROLL, EXACT, MASKED, MINB, PF, OPT>);
+        cudaFuncGetAttributes(&a, fmm_rows_kernel<Ops, LPG, VEC, NV, UNROLL, EXACT, MASKED, MINB, PF, BT>);
         return;
     }
     // Warps never cooperate across a block (no shared memory, no barrier), so
@@ -32,9 +32,10 @@ inline void launch_one(const KParams& p, const Ops& ops, cudaStream_t stream) {
     static const int kThreads = [] {
         if (const char* e = std::getenv("FMM_BLOCK_THREADS")) {
             const int t = std::atoi(e);
-            if (t >= 32 && t <= 256 && t % 32 == 0) return t;
+            if (t >= 32 && t <= BT && t % 32 == 0) return t;
         }
-        auto kern = fmm_rows_kernel<Ops, LPG, VEC, NV, UNROLL, EXACT, MASKED, MINB, PF, OPT>;
+        if (BT < 256) return BT;
+        auto kern = fmm_rows_kernel<Ops, LPG, VEC, NV, UNROLL, EXACT, MASKED, MINB, PF, BT>;
         int full = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&full, kern, 256, 0) != cudaSuccess || full <= 0) return 256;
         for (int t = 32; t < 256; t *= 2) {
@@ -50,22 +51,9 @@ inline void launch_one(const KParams& p, const Ops& ops, cudaStream_t stream) {
     const int64_t warps = wide + (p.n_narrow_rows + GPW - 1) / GPW + (zero_left + kZeroRowsPerWarp - 1) / kZeroRowsPerWarp;
     if (warps <= 0) return;
     const int64_t blocks = (warps + (kThreads / 32) - 1) / (kThreads / 32);
-    fmm_rows_kernel<Ops, LPG, VEC, NV, UNROLL, EXACT, MASKED, MINB, PF, OPT>
+    fmm_rows_kernel<Ops, LPG, VEC, NV, UNROLL, EXACT, MASKED, MINB, PF, BT>
         <<<static_cast<unsigned>(blocks), kThreads, 0, stream>>>(p, ops);
 }
-
-#ifdef FMM_TUNING_VARIANTS
-// variants 40 + OPT (OPT = 1..15): the default shape with row-kernel option bits
-template <class Ops, int LPG, int VEC, int NV, int U, int MINB, int PF, int O = 1>
-inline bool launch_opt(const KParams& p, const Ops& ops, int opt, cudaStream_t s) {
-    if constexpr (O > 15 || !(std::is_same_v<Ops, OpsSigmoid> || std::is_same_v<Ops, OpsTdist>)) {
-        return false;
-    } else {
-        if (opt == O) { launch_one<Ops, LPG, VEC, NV, U, false, false, MINB, PF, O>(p, ops, s); return true; }
-        return launch_opt<Ops, LPG, VEC, NV, U, MINB, PF, O + 1>(p, ops, opt, s);
-    }
-}
-#endif
 
 // Vectorised shapes: d = LPG * VEC * NV exactly, rows VEC*4-byte aligned.
 // variant < 0 selects the default shape for d. The shipped library holds the
@@ -93,11 +81,14 @@ inline bool launch_aligned32(const KParams& p, const Ops& ops, int d, int varian
                 if (variant == 28) { launch_one<Ops, 4, 8, 1, 2, EXACT, false, 6, 1>(p, ops, s); return true; }
                 if (variant == 29) { launch_one<Ops, 8, 4, 1, 2, EXACT, false, 6, 1>(p, ops, s); return true; }
                 if (variant == 30) { launch_one<Ops, 8, 4, 1, 4, EXACT, false, 5, 1>(p, ops, s); return true; }
-                if (variant >= 40 && launch_opt<Ops, 4, 4, 2, 2, 4, 1>(p, ops, variant - 40, s)) return true;
-                if (variant == 56) { launch_one<Ops, 4, 4, 2, 2, EXACT, false, 3, 1, 16>(p, ops, s); return true; }
-                if (variant == 57) { launch_one<Ops, 4, 4, 2, 1, EXACT, false, 4, 1, 16>(p, ops, s); return true; }
-                if (variant == 58) { launch_one<Ops, 4, 8, 1, 2, EXACT, false, 3, 1, 16>(p, ops, s); return true; }
-                if (variant == 59) { launch_one<Ops, 4, 8, 1, 1, EXACT, false, 4, 1, 16>(p, ops, s); return true; }
+                if (variant == 56) { launch_one<Ops, 4, 4, 2, 4, EXACT, false, 32, 1, 32>(p, ops, s); return true; }
+                if (variant == 57) { launch_one<Ops, 4, 8, 1, 4, EXACT, false, 28, 1, 32>(p, ops, s); return true; }
+                if (variant == 58) { launch_one<Ops, 4, 4, 2, 8, EXACT, false, 18, 1, 32>(p, ops, s); return true; }
+                if (variant == 59) { launch_one<Ops, 4, 8, 1, 4, EXACT, false, 24, 1, 32>(p, ops, s); return true; }
+                if (variant == 60) { launch_one<Ops, 4, 4, 2, 4, EXACT, false, 24, 1, 32>(p, ops, s); return true; }
+                if (variant == 61) { launch_one<Ops, 4, 4, 2, 4, EXACT, false, 28, 1, 32>(p, ops, s); return true; }
+                if (variant == 62) { launch_one<Ops, 4, 4, 2, 4, EXACT, false, 26, 1, 32>(p, ops, s); return true; }
+                if (variant == 63) { launch_one<Ops, 4, 4, 2, 4, EXACT, false, 30, 1, 32>(p, ops, s); return true; }
             }
 #endif
             // config 3 keeps the VEC = 4 shape (0.616 ms; VEC = 8 U = 2: 0.618)
@@ -111,11 +102,10 @@ inline bool launch_aligned32(const KParams& p, const Ops& ops, int d, int varian
                 if (variant == 22) { launch_one<Ops, 16, 8, 1, 4, EXACT, false>(p, ops, s); return true; }
                 if (variant == 23) { launch_one<Ops, 8, 8, 2, 2, EXACT, false>(p, ops, s); return true; }
                 if (variant == 24) { launch_one<Ops, 8, 8, 2, 4, EXACT, false, 3>(p, ops, s); return true; }
-                if (variant >= 40 && launch_opt<Ops, 8, 8, 2, 4, 2, -1>(p, ops, variant - 40, s)) return true;
-                if (variant == 56) { launch_one<Ops, 8, 8, 2, 2, EXACT, false, 2, -1, 16>(p, ops, s); return true; }
-                if (variant == 57) { launch_one<Ops, 8, 8, 2, 2, EXACT, false, 0, -1, 16>(p, ops, s); return true; }
-                if (variant == 58) { launch_one<Ops, 8, 8, 2, 1, EXACT, false, 3, -1, 16>(p, ops, s); return true; }
-                if (variant == 59) { launch_one<Ops, 8, 8, 2, 4, EXACT, false, 0, -1, 16>(p, ops, s); return true; }
+                if (variant == 60) { launch_one<Ops, 8, 8, 2, 4, EXACT, false, 15, -1, 32>(p, ops, s); return true; }
+                if (variant == 61) { launch_one<Ops, 8, 8, 2, 4, EXACT, false, 17, -1, 32>(p, ops, s); return true; }
+                if (variant == 62) { launch_one<Ops, 8, 8, 2, 4, EXACT, false, 16, -1, 32>(p, ops, s); return true; }
+                if (variant == 63) { launch_one<Ops, 16, 8, 1, 8, EXACT, false, 18, -1, 32>(p, ops, s); return true; }
 #endif
                 launch_one<Ops, 8, 8, 2, 4, EXACT, false>(p, ops, s); return true;  // config 2
             }
@@ -126,9 +116,10 @@ inline bool launch_aligned32(const KParams& p, const Ops& ops, int d, int varian
                 if (variant == 21) { launch_one<Ops, 16, 8, 2, 4, EXACT, false>(p, ops, s); return true; }
                 if (variant == 22) { launch_one<Ops, 8, 8, 4, 2, EXACT, false>(p, ops, s); return true; }
                 if (variant == 25) { launch_one<Ops, 32, 8, 1, 8, EXACT, false>(p, ops, s); return true; }
-                if (variant >= 40 && launch_opt<Ops, 32, 8, 1, 4, 0, -1>(p, ops, variant - 40, s)) return true;
-                if (variant == 56) { launch_one<Ops, 32, 8, 1, 2, EXACT, false, 3, -1, 16>(p, ops, s); return true; }
-                if (variant == 57) { launch_one<Ops, 32, 8, 1, 4, EXACT, false, 2, -1, 16>(p, ops, s); return true; }
+                if (variant == 60) { launch_one<Ops, 32, 8, 1, 8, EXACT, false, 18, -1, 32>(p, ops, s); return true; }
+                if (variant == 61) { launch_one<Ops, 32, 8, 1, 8, EXACT, false, 16, -1, 32>(p, ops, s); return true; }
+                if (variant == 62) { launch_one<Ops, 32, 8, 1, 4, EXACT, false, 28, -1, 32>(p, ops, s); return true; }
+                if (variant == 63) { launch_one<Ops, 32, 8, 1, 4, EXACT, false, 21, -1, 32>(p, ops, s); return true; }
 #endif
                 // config 5: a warp per row-group of 32 lanes x 32 B (80 registers)
                 launch_one<Ops, 32, 8, 1, 4, EXACT, false>(p, ops, s); return true;
@@ -163,9 +154,13 @@ inline bool launch_aligned(const KParams& p, const Ops& ops, int d, int variant,
                 if (variant == 4) { launch_one<Ops, 4, 4, 2, 8, EXACT, false>(p, ops, s); return true; }
                 if (variant == 8) { launch_one<Ops, 4, 4, 2, 4, EXACT, false, 4, 1>(p, ops, s); return true; }
 #endif
-                // config 3: U = 2 at 4 blocks/SM (32 warps) with the column
-                // prefetch (0.616 ms; U = 4 at 3 blocks/SM: 0.646 ms)
-                launch_one<Ops, 4, 4, 2, 2, EXACT, false, 4, 1>(p, ops, s); return true;
+                // config 3: U = 4 at 72 registers / 28 one-warp blocks per SM
+                // with the column prefetch (r3j: 0.412 ms; U = 2 at 64
+                // registers / 32 warps: 0.442 ms; U = 4 at 80 / 25: 0.426 ms)
+#ifdef FMM_TUNING_VARIANTS
+                if (variant == 9) { launch_one<Ops, 4, 4, 2, 2, EXACT, false, 4, 1>(p, ops, s); return true; }
+#endif
+                launch_one<Ops, 4, 4, 2, 4, EXACT, false, 28, 1, 32>(p, ops, s); return true;
             }
             launch_one<Ops, 4, 4, 2, 4, EXACT, false>(p, ops, s); return true;
         case 64:

@@ -39,13 +39,6 @@ constexpr int kMaxRegDim = 1024;
 constexpr int kZeroRowsPerWarp = 64;
 constexpr int kZeroPerWideMax = 32;
 
-// Row-kernel option bits (template parameter OPT)
-constexpr int kOptFast = 1;    // full sub-batches run an unpredicated copy of the loop body
-constexpr int kOptDotIlv = 2;  // the U dot products advance interleaved
-constexpr int kOptPfL2 = 4;    // neighbour rows of the next column batch prefetched into L2
-constexpr int kOptPfL1 = 8;    // neighbour rows of the next sub-batch prefetched into L1
-constexpr int kOptPipe = 16;   // wide rows: two half-size sub-batches alternate, one in flight while the other is consumed
-
 struct PeerOut {
     float* p[kMaxPeers];
     int n;
@@ -297,15 +290,6 @@ __device__ __forceinline__ float ld_stream_f32(const float* p) {
     return v;
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
-__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
-// one prefetch per 128-byte line of a d-float row
-template <int D>
-__device__ __forceinline__ void prefetch_row_l2(const float* row) {
-#pragma unroll
-    for (int b = 0; b < D * 4; b += 128) prefetch_l2(reinterpret_cast<const char*>(row) + b);
-}
-
 // xor-butterfly over the LPR lanes of a group; every lane ends with the same
 // bits (a+b == b+a in IEEE arithmetic), so all lanes agree on h.
 template <int LPR>
@@ -362,7 +346,7 @@ __device__ __forceinline__ constexpr int transposed_lane(int u) {
 // --------------------------------------------------------------- the kernel
 // Per-edge work for U gathered neighbour rows: ROP across the group, SOP,
 // MOP, AOP into z (update_u's loop body, kernel.hpp:92-106).
-template <class Ops, int LPG, int VEC, int NV, int U, bool EXACT, bool MASKED, int OPT = 0>
+template <class Ops, int LPG, int VEC, int NV, int U, bool EXACT, bool MASKED>
 __device__ __forceinline__ void consume_edges(const Ops& ops, const KParams& p, const float (&x)[NV * VEC],
                                               float (&z)[NV * VEC], const float (&y)[U][NV * VEC],
                                               const float (&a)[U], const bool (&ok)[U],
@@ -378,37 +362,6 @@ __device__ __forceinline__ void consume_edges(const Ops& ops, const KParams& p, 
         if (!EXACT && ops.aop() == FMM_AOP_ASUM && ops.rop() != FMM_ROP_NOOP &&
             ops.rop() != FMM_ROP_RMUL && ops.mop() != FMM_MOP_SEL2ND && ops.vop() != FMM_VOP_MLP) {
             float s[U];
-            if constexpr ((OPT & kOptDotIlv) != 0) {
-                // the U x 2 accumulator chains advance together (element pair
-                // outer, edge inner): consecutive FFMA2 are independent
-                float2 acc[U][2];
-#pragma unroll
-                for (int u = 0; u < U; ++u) acc[u][0] = acc[u][1] = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int e = 0; e < NE; e += 2) {
-                    const float2 xv = make_float2(x[e], x[e + 1]);
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const float2 yv = make_float2(y[u][e], y[u][e + 1]);
-                        float2& a2 = acc[u][(e >> 1) & 1];
-                        if (ops.vop() == FMM_VOP_MUL && ops.rop() == FMM_ROP_RSUM) {
-                            a2 = __ffma2_rn(xv, yv, a2);
-                        } else {
-                            float2 t;
-                            switch (ops.vop()) {
-                                case FMM_VOP_ADD: t = __fadd2_rn(xv, yv); break;
-                                case FMM_VOP_MUL: t = __fmul2_rn(xv, yv); break;
-                                case FMM_VOP_SEL2ND: t = yv; break;
-                                default: t = __ffma2_rn(yv, make_float2(-1.f, -1.f), xv); break;  // x - y
-                            }
-                            if (ops.rop() == FMM_ROP_RSUM) a2 = __fadd2_rn(a2, t);
-                            else a2 = __ffma2_rn(t, t, a2);  // NORM / SQNORM
-                        }
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) s[u] = (acc[u][0].x + acc[u][0].y) + (acc[u][1].x + acc[u][1].y);
-            } else
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
@@ -563,7 +516,7 @@ __device__ __forceinline__ void consume_edges(const Ops& ops, const KParams& p, 
     }
 }
 
-template <int LPG, int VEC, int NV, int U, bool MASKED, bool ALLOK = false>
+template <int LPG, int VEC, int NV, int U, bool MASKED>
 __device__ __forceinline__ void gather_rows(const float* __restrict__ Y, int d, const int (&v)[U],
                                             const bool (&ok)[U], const bool (&elem_ok)[NV], int gl,
                                             float (&y)[U][NV * VEC]) {
@@ -572,7 +525,7 @@ __device__ __forceinline__ void gather_rows(const float* __restrict__ Y, int d, 
         const float* yr = Y + static_cast<int64_t>(v[u]) * d;
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
-            if ((ALLOK || ok[u]) && elem_ok[i]) {
+            if (ok[u] && elem_ok[i]) {
                 load_vec<VEC>(&y[u][i * VEC], yr + (i * LPG + gl) * VEC);
             } else {
 #pragma unroll
@@ -627,9 +580,11 @@ __device__ __forceinline__ void fill_identity_rows(const KParams& p, const Ops& 
 // and the GPW partial z are combined by an xor-butterfly in fixed order.
 // Lane layout: element j = (i*LPG + lane_in_group)*VEC + c.
 // MINB = 0 leaves the register budget to ptxas (as __launch_bounds__(256));
-// MINB > 0 asks for that many resident blocks per SM (tuning variants).
-template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED, int MINB = 0, int PF = -1, int OPT = 0>
-__global__ void __launch_bounds__(256, MINB)
+// MINB > 0 asks for that many resident blocks of BT threads per SM. Warps are
+// independent, so BT = 32 with MINB = w sets the register budget for w warps
+// per SM in steps of one warp (d = 32: 72 registers, 28 warps).
+template <class Ops, int LPG, int VEC, int NV, int UNROLL, bool EXACT, bool MASKED, int MINB = 0, int PF = -1, int BT = 256>
+__global__ void __launch_bounds__(BT, MINB)
 fmm_rows_kernel(const KParams p, const Ops ops) {
     constexpr int NE = NV * VEC;
     constexpr int GPW = 32 / LPG;
@@ -640,10 +595,6 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
     // registers cost more than the hidden index latency (measured).
     // PF: -1 = this rule, 0 / 1 = forced (tuning variants)
     constexpr bool kPrefetchCols = PF >= 0 ? (PF == 1) : (!EXACT && !MASKED && (LPG * VEC * NV >= 128));
-    constexpr bool kFast = (OPT & kOptFast) != 0 && !EXACT && !MASKED;
-    constexpr bool kPfL2 = (OPT & kOptPfL2) != 0 && kPrefetchCols && !MASKED;
-    constexpr bool kPfL1 = (OPT & kOptPfL1) != 0 && kPrefetchCols && !MASKED;
-    constexpr bool kPipe = (OPT & kOptPipe) != 0 && kPrefetchCols && !MASKED && !EXACT;
 
     const int lane = threadIdx.x & 31;
     const int gl = lane & (LPG - 1);
@@ -744,53 +695,6 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
                 fill_identity_rows<Ops, LPG, VEC, NV, MASKED>(
                     p, ops, zs, static_cast<int>(min(static_cast<int64_t>(p.zero_per_wide), p.n_zero_piggy - zs)));
         }
-        if constexpr (kPipe && KPL == 1) {
-            // software pipeline over sub-batches t = 0 .. T-1 of SB edges: the
-            // gathers of t+1 are issued before t is consumed, into the other
-            // of two register buffers (same registers as one sub-batch of 2U)
-            int cidx = cnext[0];
-            float aval = anext[0];
-            int ib = 0;  // first edge of the column batch held in cidx
-            if (B < n) fetch(B);
-            const int T = (n + SB - 1) / SB;
-            auto issue = [&](int t, float (&y)[U][NE], float (&a)[U]) {
-                const int e = t * SB;
-                if (e >= ib + B) {
-                    cidx = cnext[0];
-                    aval = anext[0];
-                    ib += B;
-                    if (ib + B < n) fetch(ib + B);
-                }
-                const int s = e - ib;
-                int v[U];
-                bool ok[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int src = ((s + u * GPW) % 32) + g;
-                    v[u] = __shfl_sync(0xffffffffu, cidx, src);
-                    a[u] = has_val ? __shfl_sync(0xffffffffu, aval, src) : 1.0f;
-                    ok[u] = (e + u * GPW + g) < n;
-                }
-                gather_rows<LPG, VEC, NV, U, MASKED>(p.Y, d, v, ok, elem_ok, gl, y);
-            };
-            auto consume = [&](int t, const float (&y)[U][NE], const float (&a)[U]) {
-                bool ok[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) ok[u] = (t * SB + u * GPW + g) < n;
-                consume_edges<Ops, LPG, VEC, NV, U, EXACT, MASKED, OPT>(ops, p, x, z, y, a, ok, elem_ok);
-            };
-            float ya[U][NE], yb[U][NE], aa[U], ab[U];
-            if (T > 0) issue(0, ya, aa);
-#pragma unroll 1
-            for (int t = 0; t < T; t += 2) {
-                if (t + 1 < T) issue(t + 1, yb, ab);
-                consume(t, ya, aa);
-                if (t + 1 < T) {
-                    if (t + 2 < T) issue(t + 2, ya, aa);
-                    consume(t + 1, yb, ab);
-                }
-            }
-        } else
         for (int base = 0; base < n; base += B) {
             if constexpr (!kPrefetchCols) fetch(base);
             int cidx[KPL];
@@ -821,42 +725,8 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
                     ok[u] = (base + bq + g) < n;
                 }
                 float y[U][NE];
-                const bool full = kFast && (base + s + SB <= n);  // warp-uniform
-                if (full) gather_rows<LPG, VEC, NV, U, MASKED, true>(p.Y, d, v, ok, elem_ok, gl, y);
-                else gather_rows<LPG, VEC, NV, U, MASKED>(p.Y, d, v, ok, elem_ok, gl, y);
-                if constexpr (kPfL2) {
-                    // the next column batch has arrived by now: its rows start
-                    // towards L2 a sub-batch (or more) before they are gathered
-                    if (s == 0 && base + B < n) {
-#pragma unroll
-                        for (int q = 0; q < KPL; ++q)
-                            if (base + B + q * 32 + lane < n)
-                                prefetch_row_l2<LPG * VEC * NV>(p.Y + static_cast<int64_t>(cnext[q]) * d);
-                    }
-                }
-                if constexpr (kPfL1 && KPL == 1) {
-                    // rows of the following sub-batch into L1
-                    const int sn = s + SB;
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int bq = sn + u * GPW;
-                        const int c = bq < B ? __shfl_sync(0xffffffffu, cidx[0], (bq % 32) + g)
-                                             : __shfl_sync(0xffffffffu, cnext[0], ((bq - B) % 32) + g);
-                        if (base + bq + g < n) {
-                            const float* yr = p.Y + static_cast<int64_t>(c) * d;
-#pragma unroll
-                            for (int i = 0; i < NV; ++i) prefetch_l1(yr + (i * LPG + gl) * VEC);
-                        }
-                    }
-                }
-                if (full) {
-                    bool okt[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) okt[u] = true;
-                    consume_edges<Ops, LPG, VEC, NV, U, EXACT, MASKED, OPT>(ops, p, x, z, y, a, okt, elem_ok);
-                } else {
-                    consume_edges<Ops, LPG, VEC, NV, U, EXACT, MASKED, OPT>(ops, p, x, z, y, a, ok, elem_ok);
-                }
+                gather_rows<LPG, VEC, NV, U, MASKED>(p.Y, d, v, ok, elem_ok, gl, y);
+                consume_edges<Ops, LPG, VEC, NV, U, EXACT, MASKED>(ops, p, x, z, y, a, ok, elem_ok);
             }
         }
         // fold the GPW group partials (fixed butterfly order -> deterministic)
@@ -999,38 +869,8 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
                     ok[u] = (base + b) < n;
                 }
                 float y[U][NE];
-                const bool full = kFast && __all_sync(0xffffffffu, base + u0 + U <= n);
-                if (full) gather_rows<LPG, VEC, NV, U, MASKED, true>(p.Y, d, v, ok, elem_ok, gl, y);
-                else gather_rows<LPG, VEC, NV, U, MASKED>(p.Y, d, v, ok, elem_ok, gl, y);
-                if constexpr (kPfL2) {
-                    if (u0 == 0 && base + B < nmax) {
-#pragma unroll
-                        for (int q = 0; q < KPL; ++q)
-                            if (base + B + q * LPG + gl < n)
-                                prefetch_row_l2<LPG * VEC * NV>(p.Y + static_cast<int64_t>(cnext[q]) * d);
-                    }
-                }
-                if constexpr (kPfL1 && KPL == 1) {
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int b = u0 + U + u;
-                        const int c = b < B ? __shfl_sync(0xffffffffu, cidx[0], gbase + (b % LPG))
-                                            : __shfl_sync(0xffffffffu, cnext[0], gbase + ((b - B) % LPG));
-                        if (base + b < n) {
-                            const float* yr = p.Y + static_cast<int64_t>(c) * d;
-#pragma unroll
-                            for (int i = 0; i < NV; ++i) prefetch_l1(yr + (i * LPG + gl) * VEC);
-                        }
-                    }
-                }
-                if (full) {
-                    bool okt[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) okt[u] = true;
-                    consume_edges<Ops, LPG, VEC, NV, U, EXACT, MASKED, OPT>(ops, p, x, z, y, a, okt, elem_ok);
-                } else {
-                    consume_edges<Ops, LPG, VEC, NV, U, EXACT, MASKED, OPT>(ops, p, x, z, y, a, ok, elem_ok);
-                }
+                gather_rows<LPG, VEC, NV, U, MASKED>(p.Y, d, v, ok, elem_ok, gl, y);
+                consume_edges<Ops, LPG, VEC, NV, U, EXACT, MASKED>(ops, p, x, z, y, a, ok, elem_ok);
             }
         }
         if (active) {
