@@ -89,6 +89,7 @@ struct GShard {
     int64_t edge_begin = 0;  // first edge of the shard in the uploaded CSR
     int64_t row_begin = 0, row_end = 0, nnz = 0;
     int64_t n_split_rows = 0, n_wide_rows = 0, n_chunks = 0, n_slots = 0, nonempty = 0, max_degree = 0;
+    int64_t n_wide_at[fmm::kWideLevels] = {};  // unsplit rows with degree >= 64 << k
     int64_t* row_ptr = nullptr;
     int32_t* col = nullptr;
     float* val = nullptr;
@@ -352,8 +353,9 @@ int launch_shard(GShard& gs, const fmm_opspec& spec, int pattern, int64_t d, boo
         p.n_chunk_items = gs.n_chunks;
         p.order = gs.order + gs.n_split_rows;
         p.items = gs.items + gs.n_split_rows;
-        p.n_wide_rows = gs.n_wide_rows;
-        p.n_narrow_rows = rows - gs.n_split_rows - gs.n_wide_rows;
+        // rows a whole warp folds: the threshold depends on d (fmm_plan.h)
+        p.n_wide_rows = gs.n_wide_at[fmm::wide_level_for(gs.chunk, static_cast<int>(d))];
+        p.n_narrow_rows = rows - gs.n_split_rows - p.n_wide_rows;
     } else {
         // exact scheme: every row folded by one lane group, storage order
         p.chunks = nullptr;
@@ -840,6 +842,7 @@ fmm_status fmm_graph_upload(fmm_ctx* ctx, int64_t m, int64_t n, const int64_t* r
         gs.edge_begin = P.edge_begin;
         gs.n_split_rows = P.n_split_rows;
         gs.n_wide_rows = P.n_wide_rows;
+        for (int k = 0; k < fmm::kWideLevels; ++k) gs.n_wide_at[k] = P.n_wide_at[k];
         gs.n_chunks = static_cast<int64_t>(P.chunks.size());
         gs.n_slots = P.n_slots;
         gs.nonempty = P.nonempty_rows;

@@ -19,6 +19,17 @@ int wide_min(int chunk) {
     return std::max(64, std::min(kWideMin, chunk / 16));
 }
 
+int wide_level_for(int chunk, int d) {
+    static const int env = [] {
+        const char* e = std::getenv("FMM_WIDE");
+        return e ? std::atoi(e) : 0;
+    }();
+    int thr = env > 0 ? env : std::max(64, std::min(d >= 64 ? 512 : 128, chunk / 4));
+    int k = 0;
+    while (k + 1 < kWideLevels && (64 << (k + 1)) <= thr) ++k;
+    return k;
+}
+
 int choose_chunk_edges(int64_t total_nnz) {
     if (const char* e = std::getenv("FMM_CHUNK")) {
         const int v = std::atoi(e);
@@ -118,7 +129,10 @@ ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t ro
         if (deg > 0) ++P.nonempty_rows;
         P.max_degree = std::max(P.max_degree, deg);
         if (deg > P.chunk) ++P.n_split_rows;
-        else if (deg >= P.wide) ++P.n_wide_rows;
+        else {
+            if (deg >= P.wide) ++P.n_wide_rows;
+            for (int k = 0; k < kWideLevels && deg >= (64 << k); ++k) ++P.n_wide_at[k];
+        }
         ++count[key_of(r) + 1];
     }
     for (int k = 0; k < kKeys; ++k) count[k + 1] += count[k];

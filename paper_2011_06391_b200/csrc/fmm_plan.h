@@ -32,6 +32,16 @@ int choose_chunk_edges(int64_t total_nnz);
 constexpr int kWideMin = 512;
 // FMM_WIDE (power of two >= 8, tuning) overrides; read once.
 int wide_min(int chunk);
+// The threshold the row kernels use depends on d (r3k): a d = 128 row of a
+// few hundred edges runs ~5% faster folded by one of the warp's four lane
+// groups (the prologue latencies are shared by four rows) than spread over
+// the warp, while the eight groups of a d = 32 warp want rows of 128 edges
+// up spread. The plan counts the warp-item prefix for every power-of-two
+// threshold 64 << k, k < kWideLevels, and the launch picks one by d; the
+// rule depends on (chunk, d) only, never on the shard, so results stay
+// bitwise independent of the shard count.
+constexpr int kWideLevels = 6;  // 64, 128, 256, 512, 1024, 2048
+int wide_level_for(int chunk, int d);
 
 struct Int4 {
     int32_t x, y, z, w;
@@ -71,6 +81,7 @@ struct ShardPlan {
     std::vector<Int4> items;
     int64_t n_split_rows = 0;             // prefix of `order` cut into chunks
     int64_t n_wide_rows = 0;              // next rows with degree >= wide
+    int64_t n_wide_at[kWideLevels] = {};  // ... with degree >= 64 << k
     std::vector<Int4> chunks;             // {row, k, slot, split-row index}
     std::vector<Int4> split_rows;         // {row, first slot, nchunks, 0}
     int64_t n_slots = 0;
