@@ -823,6 +823,9 @@ fmm_status fmm_graph_upload(fmm_ctx* ctx, int64_t m, int64_t n, const int64_t* r
     // chunk size from the whole matrix (never the uploaded range or a shard):
     // per-rank uploads of one graph must split rows identically
     const int chunk = fmm::choose_chunk_edges(row_ptr[m] - row_ptr[0]);
+    // column bands for the heavy rows of graphs far larger than the L2 (also a
+    // function of the whole matrix only)
+    const fmm::BandParams bands = fmm::choose_bands(n);
     fmm_status st = FMM_OK;
     for (int s = 0; s < S && st == FMM_OK; ++s) {
         GShard& gs = g->shards[s];
@@ -832,7 +835,7 @@ fmm_status fmm_graph_upload(fmm_ctx* ctx, int64_t m, int64_t n, const int64_t* r
         gs.row_end = row_begin + bounds[s + 1];
         fmm::ShardPlan P;
         try {
-            P = fmm::build_shard_plan(row_ptr, gs.row_begin, gs.row_end, chunk);
+            P = fmm::build_shard_plan(row_ptr, gs.row_begin, gs.row_end, chunk, col_idx, bands);
         } catch (const std::exception& e) {
             st = set_err(ctx, FMM_E_UNSUPPORTED, e.what());
             break;

@@ -61,7 +61,7 @@ struct KParams {
     const int32_t* order;    // rows, heavy first: wide rows then narrow rows
     const int4* items;       // per order slot {row, e0 lo, e0 hi, degree}: one
                              // load replaces order[i] -> row_ptr[r], row_ptr[r+1]
-    const int4* chunks;      // chunk items {row, k, slot, split-row index}
+    const int4* chunks;      // chunk items {split-row index, first edge (row-relative), edges, slot}, band-major
     // in-kernel chunk fold: the warp finishing a split row's last chunk
     // (ticket from split_count) folds the row's partials in chunk order
     const int4* split_rows;  // {row, first slot, nchunks, 0}
@@ -621,11 +621,11 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
     if (wide) {
         active = true;
         if (warp < p.n_chunk_items) {
-            const int4 c = p.chunks[warp];
-            r = c.x;
-            e0 = p.row_ptr[r] + static_cast<int64_t>(c.y) * p.chunk;
-            e1 = min(e0 + static_cast<int64_t>(p.chunk), p.row_ptr[r + 1]);
-            out = p.partial + static_cast<int64_t>(c.z) * (MASKED ? p.d : LPG * VEC * NV);
+            const int4 c = __ldg(p.chunks + warp);  // {split-row index, first edge, edges, slot}
+            r = __ldg(p.split_rows + c.x).x;
+            e0 = p.row_ptr[r] + c.y;
+            e1 = e0 + c.z;
+            out = p.partial + static_cast<int64_t>(c.w) * (MASKED ? p.d : LPG * VEC * NV);
         } else {
             const int4 it = __ldg(p.items + (warp - p.n_chunk_items));
             r = it.x;
@@ -758,7 +758,7 @@ fmm_rows_kernel(const KParams p, const Ops ops) {
         if (is_chunk && p.split_count != nullptr) {
             // last chunk of the row to finish folds all its partials, in
             // chunk order per element (deterministic, shard-independent)
-            const int si = p.chunks[warp].w;
+            const int si = __ldg(p.chunks + warp).x;
             const int4 sr = p.split_rows[si];
             __threadfence();  // this warp's partial is visible device-wide
             __syncwarp();     // ... every lane's, before lane 0 takes the ticket

@@ -30,6 +30,20 @@ int wide_level_for(int chunk, int d) {
     return k;
 }
 
+BandParams choose_bands(int64_t n) {
+    BandParams b;
+    auto env_int = [](const char* name, int64_t dflt) {
+        const char* e = std::getenv(name);
+        return e ? static_cast<int64_t>(std::atoll(e)) : dflt;
+    };
+    if (env_int("FMM_BANDS", 1) == 0) return b;
+    const int64_t cols = env_int("FMM_BAND_COLS", 65536);
+    if (cols > 0 && n >= 64 * cols) b.band_cols = cols;
+    b.min_deg = static_cast<int>(std::max<int64_t>(64, env_int("FMM_BAND_MINDEG", b.min_deg)));
+    b.min_len = static_cast<int>(std::max<int64_t>(1, env_int("FMM_BAND_MINLEN", b.min_len)));
+    return b;
+}
+
 int choose_chunk_edges(int64_t total_nnz) {
     if (const char* e = std::getenv("FMM_CHUNK")) {
         const int v = std::atoi(e);
@@ -101,8 +115,11 @@ inline int degree_bucket(int64_t deg) {
 }
 }  // namespace
 
-ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t row_end, int chunk) {
+ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t row_end, int chunk,
+                           const int64_t* col_idx, BandParams bands) {
     ShardPlan P;
+    const bool banding = bands.band_cols > 0 && col_idx != nullptr;
+    auto is_split = [&](int64_t deg) { return deg > chunk || (banding && deg >= bands.min_deg); };
     P.chunk = chunk;
     P.wide = wide_min(chunk);
     P.row_begin = row_begin;
@@ -120,7 +137,7 @@ ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t ro
     std::vector<int64_t> count(kKeys + 1, 0);
     auto key_of = [&](int64_t r) {
         const int64_t deg = P.local_row_ptr[r + 1] - P.local_row_ptr[r];
-        const int split = deg > P.chunk ? 1 : 0;
+        const int split = is_split(deg) ? 1 : 0;
         // descending: larger key first
         return kKeys - 1 - (split * kBuckets + degree_bucket(deg));
     };
@@ -128,7 +145,7 @@ ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t ro
         const int64_t deg = P.local_row_ptr[r + 1] - P.local_row_ptr[r];
         if (deg > 0) ++P.nonempty_rows;
         P.max_degree = std::max(P.max_degree, deg);
-        if (deg > P.chunk) ++P.n_split_rows;
+        if (is_split(deg)) ++P.n_split_rows;
         else {
             if (deg >= P.wide) ++P.n_wide_rows;
             for (int k = 0; k < kWideLevels && deg >= (64 << k); ++k) ++P.n_wide_at[k];
@@ -164,19 +181,69 @@ ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t ro
                       static_cast<int32_t>(e0 >> 32), static_cast<int32_t>(deg)};
     }
 
-    // chunk items for the split prefix, slots assigned row by row
+    // chunk items for the split prefix, slots assigned row by row; the items
+    // then run band-major (a fixed-size chunk counts under its first column's
+    // band when the columns are at hand, else under its index)
     int64_t slot = 0;
     P.split_rows.reserve(static_cast<size_t>(P.n_split_rows));
+    std::vector<int64_t> item_band;
+    std::vector<std::pair<int32_t, int32_t>> pieces;  // {first edge (row-relative), edges}
     for (int64_t i = 0; i < P.n_split_rows; ++i) {
         const int32_t r = P.order[i];
         const int64_t deg = P.local_row_ptr[r + 1] - P.local_row_ptr[r];
-        const int64_t nch = (deg + P.chunk - 1) / P.chunk;
+        const int64_t* c = col_idx ? col_idx + P.edge_begin + P.local_row_ptr[r] : nullptr;
+        pieces.clear();
+        bool banded = banding && deg >= bands.min_deg;
+        if (banded) {
+            auto band_of = [&](int64_t col) { return col < 0 ? int64_t(0) : col / bands.band_cols; };
+            int64_t start = 0, cur = band_of(c[0]);
+            for (int64_t e = 1; e < deg && banded; ++e) {
+                if (c[e] < c[e - 1]) { banded = false; break; }  // unsorted row: fixed chunks
+                const int64_t b = band_of(c[e]);
+                if (b != cur) {
+                    if (e - start >= bands.min_len) {
+                        pieces.push_back({static_cast<int32_t>(start), static_cast<int32_t>(e - start)});
+                        start = e;
+                    }
+                    cur = b;
+                }
+            }
+            if (banded) {
+                if (deg - start < bands.min_len && !pieces.empty()) pieces.back().second += static_cast<int32_t>(deg - start);
+                else pieces.push_back({static_cast<int32_t>(start), static_cast<int32_t>(deg - start)});
+                ++P.n_banded_rows;
+            } else {
+                pieces.clear();
+            }
+        }
+        if (!banded) pieces.push_back({0, static_cast<int32_t>(deg)});
+        // no piece longer than the chunk size
+        int64_t nch = 0;
+        for (const auto& pc : pieces) nch += (pc.second + P.chunk - 1) / P.chunk;
         if (slot + nch > INT32_MAX) throw std::invalid_argument("too many chunk slots");
         const int32_t si = static_cast<int32_t>(P.split_rows.size());
         P.split_rows.push_back({r, static_cast<int32_t>(slot), static_cast<int32_t>(nch), 0});
-        for (int64_t k = 0; k < nch; ++k)
-            P.chunks.push_back({r, static_cast<int32_t>(k), static_cast<int32_t>(slot + k), si});
+        int64_t k = 0;
+        for (const auto& pc : pieces)
+            for (int32_t off = 0; off < pc.second; off += P.chunk, ++k) {
+                const int32_t e0 = pc.first + off;
+                const int32_t len = std::min<int32_t>(P.chunk, pc.second - off);
+                P.chunks.push_back({si, e0, len, static_cast<int32_t>(slot + k)});
+                item_band.push_back(c && banding ? std::max<int64_t>(c[e0], 0) / bands.band_cols : 0);
+            }
         slot += nch;
+    }
+    if (banding && P.n_banded_rows > 0) {
+        // band-major, longest first inside a band; stable on (row, piece) order
+        std::vector<int64_t> idx(P.chunks.size());
+        for (size_t q = 0; q < idx.size(); ++q) idx[q] = static_cast<int64_t>(q);
+        std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
+            if (item_band[a] != item_band[b]) return item_band[a] < item_band[b];
+            return P.chunks[a].z > P.chunks[b].z;
+        });
+        std::vector<Int4> sorted(P.chunks.size());
+        for (size_t q = 0; q < idx.size(); ++q) sorted[q] = P.chunks[idx[q]];
+        P.chunks.swap(sorted);
     }
     P.n_slots = slot;
     return P;

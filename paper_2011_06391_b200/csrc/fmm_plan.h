@@ -47,6 +47,27 @@ struct Int4 {
     int32_t x, y, z, w;
 };
 
+// Column bands (r3q). On a graph whose X is far larger than the L2 (config
+// 5: 17 GB against 126 MB) a heavy row's gathers mostly miss. When the rows of
+// at least `min_deg` edges are cut at fixed COLUMN boundaries (bands of
+// `band_cols` columns: 64 MB of d = 256 rows) and the pieces run band by band,
+// every warp on the GPU gathers from the same band at the same time, so an X
+// row is fetched from DRAM once per band sweep and then served by L2 to every
+// heavy row that references it. A piece closes at a band boundary once it has
+// `min_len` edges (sparse bands merge forward) and never exceeds the chunk
+// size. Rows must have ascending columns (CSR from csr_from_coo has); a row
+// that does not falls back to fixed-size chunks. The boundaries depend on the
+// row's own columns and on (n, total nnz) only, so results stay bitwise
+// independent of the shard count.
+struct BandParams {
+    int64_t band_cols = 0;  // 0: no banding
+    int min_deg = 4096;
+    int min_len = 32;
+};
+// Bands of 65,536 columns when the graph has at least 64 of them; FMM_BANDS=0
+// disables, FMM_BAND_COLS / FMM_BAND_MINDEG / FMM_BAND_MINLEN override (tuning).
+BandParams choose_bands(int64_t n);
+
 // part1d (kernel.hpp:24-49): boundary i is the smallest row r with
 // row_ptr[r]*t >= i*nnz; rows split evenly when nnz == 0. row_ptr may be a
 // rebased sub-range (row_ptr[0] subtracted by the caller or not: the rule is
@@ -79,16 +100,20 @@ struct ShardPlan {
     // the row's first local edge: the kernels read a row's whole descriptor
     // with one 16-byte load
     std::vector<Int4> items;
-    int64_t n_split_rows = 0;             // prefix of `order` cut into chunks
+    int64_t n_split_rows = 0;             // prefix of `order` cut into chunks (degree > chunk, or banded)
+    int64_t n_banded_rows = 0;            // of those, cut at column-band boundaries
     int64_t n_wide_rows = 0;              // next rows with degree >= wide
     int64_t n_wide_at[kWideLevels] = {};  // ... with degree >= 64 << k
-    std::vector<Int4> chunks;             // {row, k, slot, split-row index}
+    std::vector<Int4> chunks;             // {split-row index, first edge (row-relative), edges, slot}, band-major
     std::vector<Int4> split_rows;         // {row, first slot, nchunks, 0}
     int64_t n_slots = 0;
     int64_t nonempty_rows = 0;
     int64_t max_degree = 0;
 };
 
-ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t row_end, int chunk);
+// col_idx (the whole matrix's columns, indexed like row_ptr's edges) is only
+// read when bands.band_cols > 0.
+ShardPlan build_shard_plan(const int64_t* row_ptr, int64_t row_begin, int64_t row_end, int chunk,
+                           const int64_t* col_idx = nullptr, BandParams bands = {});
 
 }  // namespace fmm

@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--exact", action="store_true")
     ap.add_argument("--hot", type=int, default=0,
                     help="characterisation: remap every column to col %% HOT (an L2-resident gather set)")
+    ap.add_argument("--hot-min-deg", type=int, default=0,
+                    help="with --hot: remap only the columns of rows with at least this many edges")
     a = ap.parse_args()
 
     import torch
@@ -40,7 +42,11 @@ def main():
     A, X, spec, d = w.A, w.X, w.spec, w.d
     if a.hot:
         from paper_2011_06391_b200.fusedmm import CsrMatrix
-        A = CsrMatrix(A.nrows, A.ncols, A.row_ptr, A.col_idx % a.hot, A.values)
+        cols = A.col_idx % a.hot
+        if a.hot_min_deg > 0:
+            heavy = np.repeat(np.diff(A.row_ptr) >= a.hot_min_deg, np.diff(A.row_ptr))
+            cols = np.where(heavy, cols, A.col_idx)
+        A = CsrMatrix(A.nrows, A.ncols, A.row_ptr, cols, A.values)
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)

@@ -130,3 +130,85 @@ def test_weighted_shards_bitwise_equal():
         g.run_host(w.X.array, w.X.array, Zt, w.d, w.spec)
         check_exact(Zt, Z1.array)
     check_exact(F.fused_mm(w.A, w.X, w.X, w.spec, 3).array, Z1.array)
+
+
+@pytest.fixture
+def band_env(monkeypatch):
+    """Column bands on a small graph (they are chosen at upload): 64 bands of
+    64 columns, rows of 64+ edges cut at band boundaries, pieces of 4+ edges."""
+    monkeypatch.setenv("FMM_BAND_COLS", "64")
+    monkeypatch.setenv("FMM_BAND_MINDEG", "64")
+    monkeypatch.setenv("FMM_BAND_MINLEN", "4")
+    yield
+
+
+def _banded_graph(seed=11, n=4096):
+    """Power-law rows over n = 64 x 64 columns: hubs of 64..3000 edges next to
+    rows of a few edges and empty rows."""
+    rng = np.random.default_rng(seed)
+    deg = np.zeros(n, dtype=np.int64)
+    deg[rng.choice(n, 40, replace=False)] = rng.integers(64, 3000, 40)
+    light = rng.choice(n, n // 2, replace=False)
+    deg[light] = np.where(deg[light] == 0, rng.integers(1, 12, light.size), deg[light])
+    row_ptr = np.concatenate([[0], np.cumsum(deg)])
+    cols = np.concatenate([np.sort(rng.choice(n, k, replace=False)) for k in deg if k > 0])
+    return F.CsrMatrix(n, n, row_ptr, cols, None)
+
+
+@pytest.mark.parametrize("d", [32, 128, 256])
+def test_column_bands_parity_and_shard_determinism(band_env, d):
+    """Heavy rows cut at column-band boundaries (fmm_plan.h BandParams): the
+    pieces fold in row order, so the result meets the oracle tolerance and is
+    bitwise the same for 1, 2 and 3 shards; with FMM_BANDS=0 the same graph
+    runs on fixed-size chunks."""
+    A = _banded_graph()
+    X = F.DenseMatrix(A.nrows, d, np.random.default_rng(2).normal(0, 0.1, A.nrows * d))
+    spec = F.make_spec(F.App.NODE_EMBED_SIGMOID)
+    Zo = oracle.oracle_fused_mm(A, X, X, spec)
+    ctx = F.Context([0])
+    g = F.DeviceGraph(ctx, A)
+    info = g.info()
+    assert info.split_rows >= 40 and info.split_chunks > info.split_rows  # banded: many pieces per row
+    Z1 = np.zeros_like(Zo)
+    g.run_host(X.array, X.array, Z1, d, spec)
+    check_tolerance(Z1, Zo, A, X, X, spec)
+    for t in (2, 3):
+        gt = F.DeviceGraph(F.Context([0] * t), A)
+        Zt = np.zeros_like(Zo)
+        gt.run_host(X.array, X.array, Zt, d, spec)
+        check_exact(Zt, Z1)
+    # GCN (exact scheme) never splits rows: still bit-exact with bands on
+    gcn = F.make_spec(F.App.GCN_FORWARD)
+    Zg = np.zeros_like(Zo)
+    g.run_host(X.array, X.array, Zg, d, gcn)
+    check_exact(Zg, oracle.oracle_fused_mm(A, X, X, gcn))
+
+
+def test_column_bands_unsorted_row_falls_back(band_env):
+    """A heavy row whose columns are not ascending keeps fixed-size chunks;
+    the result still matches the oracle (which folds in storage order)."""
+    A = _banded_graph(seed=5)
+    deg = np.diff(A.row_ptr)
+    r = int(np.argmax(deg))
+    cols = A.col_idx.copy()
+    seg = cols[A.row_ptr[r]:A.row_ptr[r + 1]]
+    cols[A.row_ptr[r]:A.row_ptr[r + 1]] = seg[::-1]
+    B = F.CsrMatrix(A.nrows, A.ncols, A.row_ptr, cols, None)
+    X = F.DenseMatrix(B.nrows, 64, np.random.default_rng(4).normal(0, 0.1, B.nrows * 64))
+    spec = F.make_spec(F.App.NODE_EMBED_SIGMOID)
+    Z = np.zeros((B.nrows, 64), dtype=np.float32)
+    F.DeviceGraph(F.Context([0]), B).run_host(X.array, X.array, Z, 64, spec)
+    check_tolerance(Z, oracle.oracle_fused_mm(B, X, X, spec), B, X, X, spec)
+
+
+def test_column_bands_iterate_with_halo_exchange(band_env):
+    """Three halo-exchanging shards iterate a banded graph bitwise like one."""
+    A = _banded_graph(seed=7)
+    d = 32
+    X0 = np.random.default_rng(8).uniform(-1, 1, (A.nrows, d)).astype(np.float32)
+    spec = F.tdist_spec()
+    Z1 = F.iterate(A, F.DenseMatrix.wrap(X0.copy()), spec, 3, 1)
+    g = F.DeviceGraph(F.Context([0, 0, 0]), A)
+    X = X0.copy()
+    g.iterate_host(X, d, spec, 3)
+    check_exact(X, Z1.array)
