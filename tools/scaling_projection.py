@@ -11,7 +11,7 @@
 The exchange rides on the kernel's own stores, so a step is
 max(compute, ingress / bw, egress / bw). A projection, not a measurement.
 
-    python tools/scaling_projection.py > profiles/r2_scaling_projection.txt
+    python tools/scaling_projection.py > profiles/r3_scaling_projection.txt
 """
 import json
 from pathlib import Path
@@ -21,7 +21,18 @@ BW = 775e9
 
 
 def main():
-    lines = [json.loads(l) for l in (P / "r2v_shard_balance.jsonl").read_text().splitlines() if l.strip()]
+    # newest measurement of every (config, shard count, halo) wins: r2v (all
+    # configs), then the second-pass re-measurements (r3w configs 2 and 3, r3v config 5)
+    by_key = {}
+    for name in ("r2v_shard_balance.jsonl", "r3w_shard_balance_c2.jsonl", "r3w_shard_balance_c3.jsonl", "r3v_shard_balance_c5.jsonl"):
+        f = P / name
+        if not f.exists():
+            continue
+        for l in f.read_text().splitlines():
+            if l.strip().startswith("{"):
+                r = json.loads(l)
+                by_key[(r["config"], r["gpus"], bool(r.get("halo_stores")))] = r
+    lines = list(by_key.values())
     halo = {}
     for f in sorted(P.glob("r2_halo_volume_c*.jsonl")):
         for l in f.read_text().splitlines():
