@@ -38,7 +38,9 @@ BandParams choose_bands(int64_t n) {
     };
     if (env_int("FMM_BANDS", 1) == 0) return b;
     const int64_t cols = env_int("FMM_BAND_COLS", 65536);
-    if (cols > 0 && n >= 64 * cols) b.band_cols = cols;
+    // at least 128 bands: X several times the L2 at any d >= 32 (configs 2 and
+    // 3, 16-32 bands of this width, lose 7-50% to the extra pieces: r3x)
+    if (cols > 0 && n >= 128 * cols) b.band_cols = cols;
     b.min_deg = static_cast<int>(std::max<int64_t>(64, env_int("FMM_BAND_MINDEG", b.min_deg)));
     b.min_len = static_cast<int>(std::max<int64_t>(1, env_int("FMM_BAND_MINLEN", b.min_len)));
     return b;

@@ -64,7 +64,7 @@ struct BandParams {
     int min_deg = 4096;
     int min_len = 32;
 };
-// Bands of 65,536 columns when the graph has at least 64 of them; FMM_BANDS=0
+// Bands of 65,536 columns when the graph has at least 128 of them; FMM_BANDS=0
 // disables, FMM_BAND_COLS / FMM_BAND_MINDEG / FMM_BAND_MINLEN override (tuning).
 BandParams choose_bands(int64_t n);
 

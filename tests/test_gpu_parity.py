@@ -134,7 +134,7 @@ def test_weighted_shards_bitwise_equal():
 
 @pytest.fixture
 def band_env(monkeypatch):
-    """Column bands on a small graph (they are chosen at upload): 64 bands of
+    """Column bands on a small graph (they are chosen at upload): 128 bands of
     64 columns, rows of 64+ edges cut at band boundaries, pieces of 4+ edges."""
     monkeypatch.setenv("FMM_BAND_COLS", "64")
     monkeypatch.setenv("FMM_BAND_MINDEG", "64")
@@ -142,8 +142,8 @@ def band_env(monkeypatch):
     yield
 
 
-def _banded_graph(seed=11, n=4096):
-    """Power-law rows over n = 64 x 64 columns: hubs of 64..3000 edges next to
+def _banded_graph(seed=11, n=8192):
+    """Power-law rows over n = 128 x 64 columns: hubs of 64..3000 edges next to
     rows of a few edges and empty rows."""
     rng = np.random.default_rng(seed)
     deg = np.zeros(n, dtype=np.int64)
