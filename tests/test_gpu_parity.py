@@ -212,3 +212,30 @@ def test_column_bands_iterate_with_halo_exchange(band_env):
     X = X0.copy()
     g.iterate_host(X, d, spec, 3)
     check_exact(X, Z1.array)
+
+
+@pytest.mark.parametrize("d", [2, 32, 100, 128, 256])
+def test_outputs_stay_inside_z(band_env, d):
+    """Guard bands around Z: the row kernels (narrow rows, warp items, banded
+    pieces and their fold, the empty-row fill from wide-warp prologues and from
+    dedicated warps) write exactly the rows of Z and nothing around it."""
+    import torch
+    from paper_2011_06391_b200 import _lib
+    A = _banded_graph(seed=13)
+    n = A.nrows
+    rng = np.random.default_rng(14)
+    X = F.DenseMatrix(n, d, rng.normal(0, 0.1, n * d))
+    dev = torch.device("cuda", 0)
+    guard = 4096  # floats on either side
+    buf = torch.full((guard + n * d + guard,), 7.5, dtype=torch.float32, device=dev)
+    Zd = buf[guard:guard + n * d]
+    Xd = torch.from_numpy(X.array).to(dev)
+    spec = F.make_spec(F.App.NODE_EMBED_SIGMOID)
+    g = F.DeviceGraph(F.Context([0]), A)
+    g.run_device(Xd.data_ptr(), n, Xd.data_ptr(), Zd.data_ptr(), d, spec, flags=_lib.FMM_DEVICE_PTRS)
+    torch.cuda.synchronize()
+    host = buf.cpu().numpy()
+    assert (host[:guard] == 7.5).all() and (host[guard + n * d:] == 7.5).all()
+    Z = host[guard:guard + n * d].reshape(n, d)
+    assert not (Z == 7.5).any()  # every row written (empty rows get the identity)
+    check_tolerance(Z, oracle.oracle_fused_mm(A, X, X, spec), A, X, X, spec)
