@@ -116,13 +116,22 @@ inline bool launch_aligned32(const KParams& p, const Ops& ops, int d, int varian
                 if (variant == 21) { launch_one<Ops, 16, 8, 2, 4, EXACT, false>(p, ops, s); return true; }
                 if (variant == 22) { launch_one<Ops, 8, 8, 4, 2, EXACT, false>(p, ops, s); return true; }
                 if (variant == 25) { launch_one<Ops, 32, 8, 1, 8, EXACT, false>(p, ops, s); return true; }
+                if (variant == 56) { launch_one<Ops, 16, 8, 2, 4, EXACT, false, 14, -1, 32>(p, ops, s); return true; }
+                if (variant == 57) { launch_one<Ops, 16, 8, 2, 4, EXACT, false, 16, -1, 32>(p, ops, s); return true; }
+                if (variant == 58) { launch_one<Ops, 16, 8, 2, 4, EXACT, false, 12, -1, 32>(p, ops, s); return true; }
+                if (variant == 59) { launch_one<Ops, 16, 8, 2, 2, EXACT, false, 20, -1, 32>(p, ops, s); return true; }
                 if (variant == 60) { launch_one<Ops, 32, 8, 1, 8, EXACT, false, 18, -1, 32>(p, ops, s); return true; }
                 if (variant == 61) { launch_one<Ops, 32, 8, 1, 8, EXACT, false, 16, -1, 32>(p, ops, s); return true; }
                 if (variant == 62) { launch_one<Ops, 32, 8, 1, 4, EXACT, false, 28, -1, 32>(p, ops, s); return true; }
                 if (variant == 63) { launch_one<Ops, 32, 8, 1, 4, EXACT, false, 21, -1, 32>(p, ops, s); return true; }
 #endif
-                // config 5: a warp per row-group of 32 lanes x 32 B (80 registers)
-                launch_one<Ops, 32, 8, 1, 4, EXACT, false>(p, ops, s); return true;
+                // config 5: two rows per warp, 16 lanes x 64 B each, at 128
+                // registers / 16 one-warp blocks per SM (r3z, with the column
+                // bands: 92.5 ms; 32 lanes x 32 B at 80 registers: 98.9 ms)
+#ifdef FMM_TUNING_VARIANTS
+                if (variant == 26) { launch_one<Ops, 32, 8, 1, 4, EXACT, false>(p, ops, s); return true; }
+#endif
+                launch_one<Ops, 16, 8, 2, 4, EXACT, false, 16, -1, 32>(p, ops, s); return true;
             }
             launch_one<Ops, 16, 8, 2, 2, EXACT, false>(p, ops, s); return true;
         default: return false;
