@@ -424,11 +424,15 @@ def part1d(A: CsrMatrix, t: int) -> PartitionPlan:
 
 
 def row_weight_for(d: int) -> float:
-    """Per-row kernel cost in edge-equivalents for dimension d, from fits of
-    the measured shard times (tools/shard_balance.py): ~3.6 at d=32 (config
-    3), ~6 at d=128 (config 2), ~3.3 at d=256 (config 5, where the 8-shard
-    speed-up is flat for w in 2..10)."""
-    return min(8.0, 2.5 + d / 32.0)
+    """Per-row cost in edge-equivalents for dimension d, from fits of the
+    measured shard times (tools/shard_balance.py): ~3.6 at d=32 (config 3),
+    ~6 at d=128 (config 2). At d=256 (config 5 with the column bands) the
+    8-shard times fit 24 edge-equivalents per non-empty row, and every row
+    also costs a halo store per reading peer: w = 16 brings the slowest
+    shard's compute (11.8 ms) and the largest halo egress (11.4 ms at 775
+    GB/s) together, where w = 8 left the last shard sending 10.7 GB (13.8
+    ms) — profiles/r4d_partition_weights.txt."""
+    return 2.5 + d / 32.0 if d <= 128 else 16.0
 
 
 def shard_bounds(A: CsrMatrix, t: int, d: int) -> PartitionPlan:

@@ -24,7 +24,7 @@ def main():
     # newest measurement of every (config, shard count, halo) wins: r2v (all
     # configs), then the second-pass re-measurements (r3w configs 2 and 3, r3v, then r4c config 5)
     by_key = {}
-    for name in ("r2v_shard_balance.jsonl", "r3w_shard_balance_c2.jsonl", "r3w_shard_balance_c3.jsonl", "r3v_shard_balance_c5.jsonl", "r4c_shard_balance_c5.jsonl"):
+    for name in ("r2v_shard_balance.jsonl", "r3w_shard_balance_c2.jsonl", "r3w_shard_balance_c3.jsonl", "r3v_shard_balance_c5.jsonl", "r4c_shard_balance_c5.jsonl", "r4e_shard_balance_c5_w16.jsonl"):
         f = P / name
         if not f.exists():
             continue
