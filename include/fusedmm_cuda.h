@@ -183,6 +183,20 @@ fmm_status fmm_part1d(int64_t m, const int64_t* row_ptr, int t,
  * result is bitwise independent of the partition (rows are never split). */
 fmm_status fmm_part1d_weighted(int64_t m, const int64_t* row_ptr, int t,
                                double row_weight, int64_t* boundaries);
+/* Host only (no GPU): the split-row work list fmm_graph_upload would build
+ * for rows [row_begin, row_end) of this matrix — the rows cut into pieces
+ * (longer than the chunk size, or, on graphs far larger than L2, of 4096+
+ * edges cut at column-band boundaries) in launch order. pieces (may be NULL)
+ * receives up to cap entries of 4 values {row, first edge relative to the
+ * row, edges, band of the first column}. A diagnostic / test aid: the cuts
+ * depend on the row's own columns and on (n, total nnz) only, never on the
+ * row range, which is what keeps results bitwise independent of the shard
+ * count. */
+fmm_status fmm_plan_pieces(int64_t m, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                           int64_t row_begin, int64_t row_end, int64_t* chunk_edges,
+                           int64_t* n_split_rows, int64_t* n_banded_rows, int64_t* n_pieces,
+                           int64_t* pieces, int64_t cap);
+
 /* Row weight fmm_graph_upload uses to split a multi-shard context's rows
  * (default 0: the reference's part1d). */
 fmm_status fmm_set_row_weight(fmm_ctx* ctx, double row_weight);

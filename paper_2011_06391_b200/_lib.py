@@ -66,6 +66,8 @@ SIGNATURES = {
     "fmm_part1d": (C.c_int, [C.c_int64, _I64P, C.c_int, _I64P]),
     "fmm_part1d_weighted": (C.c_int, [C.c_int64, _I64P, C.c_int, C.c_double, _I64P]),
     "fmm_set_row_weight": (C.c_int, [_P, C.c_double]),
+    "fmm_plan_pieces": (C.c_int, [C.c_int64, C.c_int64, _I64P, _I64P, C.c_int64, C.c_int64, _I64P, _I64P, _I64P,
+                                  _I64P, _I64P, C.c_int64]),
     "fmm_graph_upload": (C.c_int, [_P, C.c_int64, C.c_int64, _I64P, _I64P, _FP, C.c_int64,
                                    C.c_int64, C.POINTER(_P)]),
     "fmm_graph_free": (C.c_int, [_P]),

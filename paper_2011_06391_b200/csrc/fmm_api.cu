@@ -762,6 +762,40 @@ fmm_status fmm_part1d_weighted(int64_t m, const int64_t* row_ptr, int t, double 
     return FMM_OK;
 }
 
+fmm_status fmm_plan_pieces(int64_t m, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                           int64_t row_begin, int64_t row_end, int64_t* chunk_edges,
+                           int64_t* n_split_rows, int64_t* n_banded_rows, int64_t* n_pieces,
+                           int64_t* pieces, int64_t cap) {
+    if (m < 0 || n < 0 || !row_ptr || row_begin < 0 || row_end > m || row_begin > row_end) return FMM_E_INVAL;
+    if (!fmm::validate_row_ptr(m, row_ptr).empty()) return FMM_E_INVAL;
+    try {
+        const int chunk = fmm::choose_chunk_edges(row_ptr[m] - row_ptr[0]);
+        const fmm::BandParams bands = fmm::choose_bands(n);
+        const fmm::ShardPlan P = fmm::build_shard_plan(row_ptr, row_begin, row_end, chunk, col_idx, bands);
+        if (chunk_edges) *chunk_edges = chunk;
+        if (n_split_rows) *n_split_rows = P.n_split_rows;
+        if (n_banded_rows) *n_banded_rows = P.n_banded_rows;
+        if (n_pieces) *n_pieces = static_cast<int64_t>(P.chunks.size());
+        if (pieces) {
+            const int64_t cnt = std::min<int64_t>(cap, static_cast<int64_t>(P.chunks.size()));
+            for (int64_t i = 0; i < cnt; ++i) {
+                const fmm::Int4& c = P.chunks[static_cast<size_t>(i)];
+                const int64_t row = P.split_rows[static_cast<size_t>(c.x)].x;  // shard-local
+                pieces[4 * i + 0] = row_begin + row;
+                pieces[4 * i + 1] = c.y;
+                pieces[4 * i + 2] = c.z;
+                int64_t band = 0;
+                if (bands.band_cols > 0 && col_idx)
+                    band = std::max<int64_t>(col_idx[row_ptr[row_begin + row] + c.y], 0) / bands.band_cols;
+                pieces[4 * i + 3] = band;
+            }
+        }
+    } catch (const std::exception&) {
+        return FMM_E_UNSUPPORTED;
+    }
+    return FMM_OK;
+}
+
 fmm_status fmm_set_row_weight(fmm_ctx* ctx, double row_weight) {
     if (!ctx || !(row_weight >= 0.0)) return FMM_E_INVAL;
     std::lock_guard<std::mutex> lk(ctx->mu);

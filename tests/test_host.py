@@ -157,3 +157,115 @@ def test_parity_rejects_non_finite_mismatch():
         check_tolerance(bad, Zr, A, X, X, spec)
     e = oracle.row_errors(np.array([[np.nan, 1.0]]), np.array([[np.nan, 1.0]]))
     assert e[0] == 0.0
+
+
+# ----------------------------------------------------------- work lists
+def _plan_pieces(A, rb=0, re=None):
+    import ctypes as C
+    from paper_2011_06391_b200 import _lib
+    re = A.nrows if re is None else re
+    L = _lib.lib()
+    rp = np.ascontiguousarray(A.row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(A.col_idx, dtype=np.int64)
+    p64 = lambda a: a.ctypes.data_as(C.POINTER(C.c_int64))
+    chunk, ns, nb, npc = (C.c_int64() for _ in range(4))
+    assert L.fmm_plan_pieces(A.nrows, A.ncols, p64(rp), p64(ci), rb, re, C.byref(chunk), C.byref(ns), C.byref(nb),
+                             C.byref(npc), None, 0) == 0
+    out = np.zeros((max(npc.value, 1), 4), dtype=np.int64)
+    assert L.fmm_plan_pieces(A.nrows, A.ncols, p64(rp), p64(ci), rb, re, None, None, None, None, p64(out),
+                             npc.value) == 0
+    return chunk.value, ns.value, nb.value, out[:npc.value]
+
+
+def _heavy_graph(seed, n=8192):
+    rng = np.random.default_rng(seed)
+    deg = np.zeros(n, dtype=np.int64)
+    deg[rng.choice(n, 30, replace=False)] = rng.integers(64, 2500, 30)
+    light = rng.choice(n, n // 3, replace=False)
+    deg[light] = np.where(deg[light] == 0, rng.integers(1, 10, light.size), deg[light])
+    row_ptr = np.concatenate([[0], np.cumsum(deg)])
+    cols = np.concatenate([np.sort(rng.choice(n, k, replace=False)) for k in deg if k > 0])
+    return F.CsrMatrix(n, n, row_ptr, cols, None)
+
+
+def test_plan_pieces_fixed_chunks_cover_split_rows(monkeypatch):
+    """Without column bands (small n) only rows longer than the chunk size are
+    cut, into consecutive chunk-size pieces that cover the row exactly."""
+    monkeypatch.setenv("FMM_BANDS", "0")
+    monkeypatch.setenv("FMM_CHUNK", "256")
+    A = _heavy_graph(1)
+    chunk, ns, nb, pc = _plan_pieces(A)
+    deg = np.diff(A.row_ptr)
+    assert chunk == 256 and nb == 0 and ns == int((deg > 256).sum())
+    for r in np.unique(pc[:, 0]):
+        mine = pc[pc[:, 0] == r]
+        mine = mine[np.argsort(mine[:, 1])]
+        assert mine[0, 1] == 0 and (mine[:-1, 1] + mine[:-1, 2] == mine[1:, 1]).all()
+        assert mine[:, 2].sum() == deg[r] and (mine[:-1, 2] == 256).all() and mine[-1, 2] <= 256
+
+
+def test_plan_pieces_column_bands(monkeypatch):
+    """Column bands: rows of min_deg+ edges are cut where their (ascending)
+    columns cross a band boundary once a piece has min_len edges; pieces never
+    exceed the chunk size, cover each row exactly, and launch band-major."""
+    monkeypatch.setenv("FMM_BAND_COLS", "64")
+    monkeypatch.setenv("FMM_BAND_MINDEG", "64")
+    monkeypatch.setenv("FMM_BAND_MINLEN", "4")
+    monkeypatch.setenv("FMM_CHUNK", "256")
+    A = _heavy_graph(2)
+    deg = np.diff(A.row_ptr)
+    chunk, ns, nb, pc = _plan_pieces(A)
+    assert ns == int((deg >= 64).sum()) and nb == ns and len(pc) > ns
+    assert (np.diff(pc[:, 3]) >= 0).all()  # band-major launch order
+    for r in np.unique(pc[:, 0]):
+        mine = pc[pc[:, 0] == r]
+        mine = mine[np.argsort(mine[:, 1])]
+        assert mine[0, 1] == 0 and (mine[:-1, 1] + mine[:-1, 2] == mine[1:, 1]).all()
+        assert mine[:, 2].sum() == deg[r] and (mine[:, 2] <= chunk).all()
+        cols = A.col_idx[A.row_ptr[r]:A.row_ptr[r + 1]]
+        for e0, ln, band in mine[:, 1:]:
+            assert cols[e0] // 64 == band
+            # a cut happens only at a band boundary or at the chunk size
+            if e0 > 0:
+                assert cols[e0] // 64 != cols[e0 - 1] // 64 or any(
+                    (e0 - s) % chunk == 0 for s in mine[mine[:, 1] < e0][:, 1])
+        assert (mine[:-1, 2] >= 4).all() or len(mine) == 1
+
+
+def test_plan_pieces_independent_of_the_row_range(monkeypatch):
+    """A row is cut the same way whichever shard (row range) it falls in: the
+    property behind bitwise-identical results across shard counts."""
+    monkeypatch.setenv("FMM_BAND_COLS", "64")
+    monkeypatch.setenv("FMM_BAND_MINDEG", "64")
+    monkeypatch.setenv("FMM_BAND_MINLEN", "4")
+    A = _heavy_graph(3)
+    _, _, _, whole = _plan_pieces(A)
+    key = lambda pc: sorted(map(tuple, pc[:, :3].tolist()))
+    parts = []
+    for rb, re in ((0, 3000), (3000, 5000), (5000, A.nrows)):
+        parts.append(_plan_pieces(A, rb, re)[3])
+    assert key(np.concatenate(parts)) == key(whole)
+
+
+def test_plan_pieces_unsorted_row_keeps_fixed_chunks(monkeypatch):
+    monkeypatch.setenv("FMM_BAND_COLS", "64")
+    monkeypatch.setenv("FMM_BAND_MINDEG", "64")
+    monkeypatch.setenv("FMM_CHUNK", "256")
+    A = _heavy_graph(4)
+    deg = np.diff(A.row_ptr)
+    r = int(np.argmax(deg))
+    cols = A.col_idx.copy()
+    cols[A.row_ptr[r]:A.row_ptr[r + 1]] = cols[A.row_ptr[r]:A.row_ptr[r + 1]][::-1]
+    B = F.CsrMatrix(A.nrows, A.ncols, A.row_ptr, cols, None)
+    _, ns, nb, pc = _plan_pieces(B)
+    assert nb == ns - 1
+    mine = pc[pc[:, 0] == r]
+    assert len(mine) == -(-deg[r] // 256) and (np.sort(mine[:, 1]) == np.arange(len(mine)) * 256).all()
+
+
+def test_wide_threshold_and_bands_depend_on_whole_matrix_only(monkeypatch):
+    """fmm_plan_pieces reports the chunk size chosen from the whole matrix's
+    nnz, also when asked about a sub-range."""
+    A = _heavy_graph(5)
+    c_all = _plan_pieces(A)[0]
+    assert _plan_pieces(A, 100, 200)[0] == c_all
