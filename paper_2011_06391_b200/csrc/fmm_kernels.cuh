@@ -572,9 +572,14 @@ __device__ __forceinline__ void fill_identity_rows(const KParams& p, const Ops& 
 }
 
 // Work items, in launch order (heaviest first, LPT-like):
-//   [0, n_chunk_items)                 chunk of a split row  -> wide warp
+//   [0, n_chunk_items)                 piece of a split row  -> wide warp
+//                                      (band-major when the plan cut the heavy
+//                                      rows at column-band boundaries)
 //   [.., + n_wide_rows)                row order[i]          -> wide warp
-//   then narrow rows, GPW = 32/LPG per warp, one per lane group.
+//   then narrow rows, GPW = 32/LPG per warp, one per lane group,
+//   then warps that only write the AOP identity to empty rows
+//   (kZeroRowsPerWarp each; the wide warps take the first n_zero_piggy).
+// One warp per block wherever the occupancy allows (launch_one).
 // A wide warp spreads its item's edges over the GPW groups round-robin
 // (edge k -> group k % GPW), each group folds its edges in storage order,
 // and the GPW partial z are combined by an xor-butterfly in fixed order.
