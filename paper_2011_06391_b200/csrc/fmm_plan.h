@@ -62,7 +62,7 @@ struct Int4 {
 struct BandParams {
     int64_t band_cols = 0;  // 0: no banding
     int min_deg = 4096;
-    int min_len = 32;
+    int min_len = 64;
 };
 // Bands of 65,536 columns when the graph has at least 128 of them; FMM_BANDS=0
 // disables, FMM_BAND_COLS / FMM_BAND_MINDEG / FMM_BAND_MINLEN override (tuning).
